@@ -1,0 +1,324 @@
+"""HBM residency of scene geometry and per-frame descriptors.
+
+Layout in HBM (per GPU):
+
+* geometry (uploaded once per mesh, cached on the mesh object's identity):
+  - positions: ``float32[V,3]`` when every coordinate is exactly
+    representable in float32 (12 B/vertex, the roofline layout);
+    ``float64[V,3]`` otherwise (the reference's ctx.positions);
+    ``uint16[V,3]`` for ``QuantizedPositions`` (decoded in-register).
+  - indices: ``uint32[3T]``, or the bit-packed stream of a
+    ``PackedIndexBuffer`` as little-endian 32-bit words (decoded in-register).
+* per-frame descriptors (one pinned H2D copy per frame): global-ID prefix,
+  object->view / object->world 3x4 float64 matrices from numpy (exactly the
+  reference's ``(view @ T)[:3]``, pipeline.py:101-102), the fp32 filter rows
+  with their error bounds, instancing groups and the stage-1 work table.
+* workspace (grow-only, reused across frames): visibility buffer
+  ``uint64[W*H]`` (66 MB at 4K, L2-resident), stage-2/3 queues, counters.
+"""
+
+from __future__ import annotations
+
+import math
+import weakref
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .codec import is_packed_indices, is_quantized_positions
+
+U = 2.0 ** -24
+E_FACTOR = 16.0
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise N.NativeError("no CUDA device: the B200 path has no CPU fallback")
+
+
+# --------------------------------------------------------------- geometry
+class DeviceMesh:
+    """One mesh resident on the GPU in its storage format."""
+
+    def __init__(self, mesh, device):
+        pos = mesh.positions
+        idx = mesh.indices
+        self.triangle_count = int(mesh.triangle_count)
+        self.device = device
+        if is_quantized_positions(pos):
+            self.pos_format = N.POS_U16
+            coords = np.ascontiguousarray(pos.coords, dtype=np.uint16)
+            self.positions = torch.from_numpy(coords.view(np.int16)).to(device)
+            self.qgrid = np.concatenate([np.asarray(pos.grid_min, dtype=np.float64),
+                                         np.asarray(pos.grid_size, dtype=np.float64)])
+            gmin = np.abs(self.qgrid[:3])
+            self.pos_bound = gmin + np.abs(self.qgrid[3:])
+            self.vertex_count = len(coords)
+            self._host_f64 = None
+        else:
+            p64 = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+            p32 = p64.astype(np.float32)
+            self.vertex_count = len(p64)
+            self.qgrid = np.zeros(6)
+            self.pos_bound = (np.abs(p64).max(axis=0) if len(p64) else np.zeros(3))
+            if np.array_equal(p32.astype(np.float64), p64):
+                self.pos_format = N.POS_F32
+                self.positions = torch.from_numpy(p32).to(device)
+            else:
+                self.pos_format = N.POS_F64
+                self.positions = torch.from_numpy(p64).to(device)
+        if is_packed_indices(idx):
+            self.idx_format = N.IDX_PACKED
+            data = np.asarray(idx.data, dtype=np.uint8)
+            nwords = (len(data) + 3) // 4 + 2
+            buf = np.zeros(nwords * 4, dtype=np.uint8)
+            buf[:len(data)] = data
+            self.indices = torch.from_numpy(buf.view(np.int32)).to(device)
+            self.pack = (int(idx.min_index), int(idx.bits_per_index))
+        else:
+            i32 = np.ascontiguousarray(idx, dtype=np.uint32).ravel()
+            self.idx_format = N.IDX_U32
+            self.indices = torch.from_numpy(i32.view(np.int32)).to(device)
+            self.pack = (0, 32)
+
+    def positions_as(self, fmt):
+        """Positions converted on the device to a wider common format."""
+        if fmt == self.pos_format:
+            return self.positions
+        if fmt == N.POS_F64:
+            if self.pos_format == N.POS_F32:
+                return self.positions.double()
+            q = self.positions.view(torch.int16).to(torch.int32) & 0xFFFF
+            q = q.double()
+            g = torch.from_numpy(self.qgrid).to(self.device)
+            # grid_min + (q + 0.5) / 65536.0 * grid_size  (geomcodec.py:101)
+            return g[:3] + (q + 0.5) / 65536.0 * g[3:]
+        raise ValueError("unsupported position conversion")
+
+    def indices_u32(self):
+        if self.idx_format == N.IDX_U32:
+            return self.indices
+        mn, b = self.pack
+        n = 3 * self.triangle_count
+        e = torch.arange(n, device=self.device, dtype=torch.int64)
+        bit = e * b
+        w = self.indices.to(torch.int64) & 0xFFFFFFFF
+        lo = w[bit >> 5]
+        hi = w[(bit >> 5) + 1]
+        win = lo | (hi << 32)
+        rel = (win >> (bit & 31)) & ((1 << b) - 1) if b < 63 else win
+        return (rel + mn).to(torch.int64).to(torch.int32)
+
+
+_mesh_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_mesh_cache_by_id: dict = {}
+
+
+def device_mesh(mesh, device) -> DeviceMesh:
+    """Upload (once) and return the device copy of a mesh.  The cache entry is
+    keyed on the mesh object and validated against the identity of its
+    positions/indices objects, so replacing them re-uploads."""
+    key_objs = (id(mesh.positions), id(mesh.indices), int(mesh.triangle_count), str(device))
+    try:
+        ent = _mesh_cache.get(mesh)
+    except TypeError:
+        ent = _mesh_cache_by_id.get(id(mesh))
+    if ent is not None and ent[0] == key_objs:
+        return ent[1]
+    dm = DeviceMesh(mesh, device)
+    try:
+        _mesh_cache[mesh] = (key_objs, dm)
+    except TypeError:
+        _mesh_cache_by_id[id(mesh)] = (key_objs, dm)
+    return dm
+
+
+class SceneGeometry:
+    """Concatenation of the draw list's unique meshes in one device format,
+    in first-appearance order (pipeline.py:103-111)."""
+
+    def __init__(self, meshes: list, device):
+        dms = [device_mesh(m, device) for m in meshes]
+        self.meshes = dms
+        pfs = {d.pos_format for d in dms}
+        ifs = {d.idx_format for d in dms}
+        if pfs == {N.POS_F32}:
+            self.pos_format = N.POS_F32
+        elif pfs == {N.POS_U16}:
+            self.pos_format = N.POS_U16
+        else:
+            self.pos_format = N.POS_F64
+        self.idx_format = N.IDX_PACKED if ifs == {N.IDX_PACKED} else N.IDX_U32
+        self.vtx_off = []
+        self.idx_off = []
+        pos_parts, idx_parts = [], []
+        nv = ni = 0
+        for d in dms:
+            self.vtx_off.append(nv)
+            self.idx_off.append(ni)
+            p = d.positions_as(self.pos_format)
+            pos_parts.append(p.reshape(-1))
+            ix = d.indices if self.idx_format == N.IDX_PACKED else d.indices_u32()
+            idx_parts.append(ix.reshape(-1))
+            nv += d.vertex_count
+            ni += ix.numel()
+        if len(dms) == 1:
+            self.positions = pos_parts[0]
+            self.indices = idx_parts[0]
+        else:
+            self.positions = torch.cat(pos_parts)
+            self.indices = torch.cat(idx_parts)
+        self.keepalive = dms
+
+
+_scene_cache: dict = {}
+
+
+def scene_geometry(meshes: list, device) -> SceneGeometry:
+    key = (tuple((id(m), id(m.positions), id(m.indices)) for m in meshes), str(device))
+    sg = _scene_cache.get(key)
+    if sg is not None:
+        return sg
+    if len(_scene_cache) > 8:
+        _scene_cache.clear()
+    sg = SceneGeometry(meshes, device)
+    _scene_cache[key] = sg
+    return sg
+
+
+# --------------------------------------------------------- filter constants
+def filter_rows(item_mv: np.ndarray, pos_bound: np.ndarray, p0: float, p1: float,
+                width: int, height: int, near: float) -> np.ndarray:
+    """fp32 filter block per item (curast.h CURAST_FILTER_FLOATS).
+
+    X = px*d = A*vx + B*d, Y = py*d = Dh*d - C*vy, d = -vz with
+    A = W/2*p0, B = W/2, C = H/2*p1, Dh = H/2 (kernels.py:78-96 rearranged).
+    Error bounds E = 16u * sum |term| over the item's position box."""
+    n = len(item_mv)
+    m = item_mv.reshape(n, 3, 4)
+    A = 0.5 * width * p0
+    B = 0.5 * width
+    C = 0.5 * height * p1
+    Dh = 0.5 * height
+    X = A * m[:, 0, :] - B * m[:, 2, :]
+    Y = -C * m[:, 1, :] - Dh * m[:, 2, :]
+    Dd = -m[:, 2, :]
+    P = np.concatenate([pos_bound, np.ones((n, 1))], axis=1)   # (n, 4)
+    SX = ((np.abs(A * m[:, 0, :]) + np.abs(B * m[:, 2, :])) * P).sum(axis=1)
+    SY = ((np.abs(C * m[:, 1, :]) + np.abs(Dh * m[:, 2, :])) * P).sum(axis=1)
+    SD = (np.abs(m[:, 2, :]) * P).sum(axis=1)
+    exy = E_FACTOR * U * np.maximum(SX, SY) * (1 + 2.0 ** -20) + 1e-30
+    ed = E_FACTOR * U * SD * (1 + 2.0 ** -20) + 1e-30
+    near_hi = np.maximum(near + 2.0 * ed + 2.0 ** -40 * SD, 4.0 * ed)
+    out = np.zeros((n, N.FILTER_FLOATS), dtype=np.float32)
+    out[:, 0:4] = X
+    out[:, 4:8] = Y
+    out[:, 8:12] = Dd
+    out[:, 12] = _f32_up(exy)
+    out[:, 13] = _f32_up(ed)
+    out[:, 14] = _f32_up(near_hi)
+    bad = ~np.all(np.isfinite(out), axis=1)
+    if bad.any():
+        # non-finite rows never decide anything: near_hi = +inf forces fp64
+        out[bad, 14] = np.inf
+    return out
+
+
+def _f32_up(x: np.ndarray) -> np.ndarray:
+    f = np.asarray(x, dtype=np.float64).astype(np.float32)
+    lo = f.astype(np.float64) < x
+    f[lo] = np.nextafter(f[lo], np.float32(np.inf))
+    return f
+
+
+# ------------------------------------------------------------- workspace
+class Workspace:
+    """Grow-only device buffers reused across frames (no allocation on the
+    frame path once warm)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.fb = None
+        self.npix = 0
+        self.q2 = None
+        self.q2_alloc = 0
+        self.q3 = None
+        self.q3_alloc = 0
+        self.counters = torch.zeros(N.COUNTER_SLOTS, dtype=torch.int64, device=device)
+        self.counters_host = torch.zeros(N.COUNTER_SLOTS, dtype=torch.int64).pin_memory()
+
+    def framebuffer(self, npix: int, fresh: bool):
+        """Visibility buffer for a frame.  ``fresh`` returns a new tensor (the
+        caller keeps it, e.g. in a returned Framebuffer)."""
+        if fresh:
+            return torch.empty(npix, dtype=torch.int64, device=self.device)
+        if self.fb is None or self.npix != npix:
+            self.fb = torch.empty(npix, dtype=torch.int64, device=self.device)
+            self.npix = npix
+        return self.fb
+
+    def ensure_q2(self, n: int):
+        n = max(1, int(n))
+        if n > self.q2_alloc:
+            self.q2 = torch.empty(2 * n, dtype=torch.int64, device=self.device)
+            self.q2_alloc = n
+        return self.q2
+
+    def ensure_q3(self, n: int):
+        n = max(1, int(n))
+        if n > self.q3_alloc:
+            self.q3 = torch.empty(4 * n, dtype=torch.int64, device=self.device)
+            self.q3_alloc = n
+        return self.q3
+
+
+_workspaces: dict = {}
+
+
+def workspace(device) -> Workspace:
+    key = str(device)
+    ws = _workspaces.get(key)
+    if ws is None:
+        ws = Workspace(device)
+        _workspaces[key] = ws
+    return ws
+
+
+class PackedUpload:
+    """Packs many small host arrays into one pinned buffer and one H2D copy;
+    returns device tensors viewing it."""
+
+    def __init__(self):
+        self.parts = []
+
+    def add(self, arr: np.ndarray) -> int:
+        arr = np.ascontiguousarray(arr)
+        self.parts.append(arr)
+        return len(self.parts) - 1
+
+    def upload(self, device, stream=None):
+        offs = []
+        total = 0
+        for a in self.parts:
+            total = (total + 255) & ~255
+            offs.append(total)
+            total += a.nbytes
+        total = max(total, 256)
+        host = torch.empty(total, dtype=torch.uint8).pin_memory()
+        hn = host.numpy()
+        for a, o in zip(self.parts, offs):
+            hn[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
+        dev = torch.empty(total, dtype=torch.uint8, device=device)
+        dev.copy_(host, non_blocking=True)
+        self.host = host          # keep pinned source alive until the copy ran
+        self.dev = dev
+        self.offsets = offs
+        return dev
+
+    def ptr(self, k: int) -> int:
+        return self.dev.data_ptr() + self.offsets[k]
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.dev.numel())

@@ -1,0 +1,161 @@
+"""Sort-last multi-GPU rendering.
+
+One process per GPU.  Every rank builds the same host draw list (same prefix
+sums, hence the same global triangle IDs), rasterizes the contiguous global-ID
+range ``shard_range(total, world, rank)`` (or a unique-triangle range of the
+instancing groups) into its own full-resolution visibility buffer, and the
+buffers are composited with an unsigned 64-bit minimum:
+
+* on GPUs: ``ncclAllReduce`` / ``ncclReduce`` / ``ncclReduceScatter`` with
+  ``ncclUint64`` + ``ncclMin`` through libcurast_nccl.so (the communicator is
+  bootstrapped by broadcasting an ncclUniqueId over torch.distributed);
+* on CPU process groups (gloo, used by the tests): ``all_reduce(MIN)`` on the
+  words with the sign bit flipped, which maps unsigned order onto signed order
+  (CLEAR = all ones must stay the largest value; a plain int64 min would make
+  it -1 and let it win).
+
+The composite is bit-identical to a 1-GPU frame: min is associative and
+commutative and every fragment carries its global ID.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+SIGN = -0x8000000000000000
+_HERE = os.path.dirname(os.path.abspath(__file__))
+NCCL_LIB = os.path.join(_HERE, "libcurast_nccl.so")
+
+
+def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, disjoint, covering split of [0, total) (rank-major)."""
+    base, rem = divmod(int(total), int(world))
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def composite_min_u64_(words: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place unsigned-min all-reduce of int64-viewed u64 words through
+    torch.distributed (any backend that supports MIN on int64)."""
+    words ^= SIGN
+    dist.all_reduce(words, op=dist.ReduceOp.MIN, group=group)
+    words ^= SIGN
+    return words
+
+
+_nccl = None
+
+
+def nccl_lib():
+    global _nccl
+    if _nccl is None:
+        if not os.path.exists(NCCL_LIB):
+            raise N.NativeError(f"{NCCL_LIB} missing (run __graft_entry__.build())")
+        L = ctypes.CDLL(NCCL_LIB)
+        P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        L.curast_nccl_last_error.restype = ctypes.c_char_p
+        L.curast_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.curast_nccl_init.argtypes = [ctypes.POINTER(P), ctypes.c_char_p, I32, I32]
+        L.curast_nccl_destroy.argtypes = [P]
+        L.curast_nccl_allreduce_min_u64.argtypes = [P, P, I64, P]
+        L.curast_nccl_reduce_min_u64.argtypes = [P, P, P, I64, I32, P]
+        L.curast_nccl_reduce_scatter_min_u64.argtypes = [P, P, P, I64, P]
+        for fn in ("curast_nccl_unique_id", "curast_nccl_init", "curast_nccl_destroy",
+                   "curast_nccl_allreduce_min_u64", "curast_nccl_reduce_min_u64",
+                   "curast_nccl_reduce_scatter_min_u64"):
+            getattr(L, fn).restype = I32
+        _nccl = L
+    return _nccl
+
+
+def _ncheck(rc, what):
+    if rc != 0:
+        raise N.NativeError(f"{what}: {nccl_lib().curast_nccl_last_error().decode()}")
+
+
+class NcclComm:
+    """A raw NCCL communicator over the ranks of the default process group."""
+
+    def __init__(self, group=None):
+        L = nccl_lib()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        buf = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _ncheck(L.curast_nccl_unique_id(buf), "ncclGetUniqueId")
+        obj = [bytes(buf.raw)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.comm = ctypes.c_void_p()
+        _ncheck(L.curast_nccl_init(ctypes.byref(self.comm), obj[0], self.world, self.rank),
+                "ncclCommInitRank")
+
+    def allreduce_min(self, words: torch.Tensor, stream=None):
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _ncheck(nccl_lib().curast_nccl_allreduce_min_u64(self.comm, words.data_ptr(),
+                                                         words.numel(), st), "allreduce")
+
+    def reduce_min(self, words: torch.Tensor, out: torch.Tensor, root=0, stream=None):
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _ncheck(nccl_lib().curast_nccl_reduce_min_u64(self.comm, words.data_ptr(), out.data_ptr(),
+                                                      words.numel(), root, st), "reduce")
+
+    def reduce_scatter_min(self, words: torch.Tensor, stripe: torch.Tensor, stream=None):
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _ncheck(nccl_lib().curast_nccl_reduce_scatter_min_u64(
+            self.comm, words.data_ptr(), stripe.data_ptr(), stripe.numel(), st), "reduce_scatter")
+
+    def close(self):
+        if self.comm:
+            nccl_lib().curast_nccl_destroy(self.comm)
+            self.comm = None
+
+
+class Compositor:
+    """Per-frame composite of a rank's visibility buffer (int64 CUDA tensor)."""
+
+    def __init__(self, words: torch.Tensor, world: int):
+        self.words = words
+        self.world = world
+        self.launches_per_call = 1
+        if words.is_cuda and dist.get_backend() == "nccl" and os.path.exists(NCCL_LIB):
+            self.comm = NcclComm()
+        else:
+            self.comm = None
+            self.launches_per_call = 3
+
+    def allreduce_min(self):
+        if self.comm is not None:
+            self.comm.allreduce_min(self.words)
+        else:
+            composite_min_u64_(self.words)
+
+
+def render_sharded(draw_list, camera, cfg=None, *, group=None):
+    """Sort-last frame on the calling rank's GPU: rasterize this rank's
+    global-ID shard, composite over all ranks; every rank returns the full
+    composite Framebuffer and its shard's FrameStats (sum them for totals)."""
+    from .config import RasterConfig
+    from .pipeline import PreparedFrame, build_context
+    from .scene import Framebuffer
+    cfg = cfg or RasterConfig()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ctx = build_context(draw_list, camera)
+    instanced = (cfg.instancing == "on"
+                 or (cfg.instancing == "auto" and ctx.max_instances >= 2))
+    space = int(ctx.group_prefix[-1]) if instanced else int(draw_list.total_triangles)
+    lo, hi = shard_range(space, world, rank)
+    pf = PreparedFrame(draw_list, camera, cfg, ctx, work_range=(lo, hi))
+    c, secs = pf.run()
+    st = pf.stats(c, secs)
+    if world > 1:
+        comp = Compositor(pf.fb, world)
+        comp.allreduce_min()
+    return Framebuffer(camera.internal_width, camera.internal_height, device_words=pf.fb), st

@@ -1,0 +1,416 @@
+"""Drop-in ``render_frame`` / ``render_draw_list`` on the B200.
+
+Same signatures, argument meaning, return types and errors as the
+reference's ``trirast/pipeline.py:207-372``; the three stages run as sm_100a
+kernels (libcurast_b200.so) on one CUDA stream with no host synchronisation
+until the frame's counters are read back:
+
+    clear VB -> stage 1 (+ fp64 fallback) -> stage 2 -> stage 3
+
+Capacity contract (pipeline.py:281-285, 323-327): queues keep counting past
+capacity and the host raises ``CapacityError`` with the required size.  The
+reference's default capacities (config.py:32-42) are far larger than what is
+worth allocating up front (64 x T stage-3 entries), so the device starts from
+``DEVICE_Q*_INITIAL`` entries and, when a frame needs more but still fits the
+capacity the reference would resolve, grows the queue and re-runs the frame
+(the output is identical: the fragment multiset is the same).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .config import (DEVICE_Q2_INITIAL, DEVICE_Q3_INITIAL, FrameStats, RasterConfig,
+                     Stage1Stats, Stage2Stats, Stage3Stats)
+from .device import PackedUpload, filter_rows, scene_geometry, workspace
+from .scene import (CLEAR, CapacityError, DrawList, Framebuffer, build_draw_list,
+                    projection_vector)
+
+# CURAST_FILTER=0 disables the fp32 cull filter (every triangle fp64) — a
+# debugging/verification switch, not a fallback.
+_FILTER_DEFAULT = os.environ.get("CURAST_FILTER", "1") != "0"
+
+
+@dataclass
+class RenderContext:
+    """Host-side flattened per-item arrays (pipeline.py:68-84)."""
+
+    prefix: np.ndarray
+    item_mv: np.ndarray
+    item_mw: np.ndarray
+    item_vtx_off: np.ndarray
+    item_idx_off: np.ndarray
+    meshes: list
+    item_mesh: np.ndarray
+    group_prefix: np.ndarray
+    group_item_off: np.ndarray
+    group_item_count: np.ndarray
+    group_items: np.ndarray
+    max_instances: int
+
+
+def build_context(draw_list: DrawList, camera) -> RenderContext:
+    """Per-item matrices with the reference's numpy expressions
+    (pipeline.py:96-102) and the instancing groups (pipeline.py:114-135).
+    Geometry is not concatenated on the host: meshes are uploaded once and
+    concatenated on the device (device.SceneGeometry)."""
+    items = draw_list.items
+    n = len(items)
+    view = camera.view_transform
+    item_mv = np.empty((n, 3, 4))
+    item_mw = np.empty((n, 3, 4))
+    mesh_ids: dict = {}
+    meshes = []
+    item_mesh = np.empty(n, dtype=np.int64)
+    for k, it in enumerate(items):
+        item_mw[k] = it.instance_transform[:3]
+        item_mv[k] = (view @ it.instance_transform)[:3]
+        key = id(it.mesh)
+        if key not in mesh_ids:
+            mesh_ids[key] = len(meshes)
+            meshes.append(it.mesh)
+        item_mesh[k] = mesh_ids[key]
+    counts, tris, flat = [], [], []
+    k = 0
+    max_inst = 1
+    while k < n:
+        node = items[k].node_index
+        j = k
+        while j < n and items[j].node_index == node:
+            j += 1
+        flat.extend(range(k, j))
+        counts.append(j - k)
+        tris.append(items[k].triangle_count)
+        max_inst = max(max_inst, j - k)
+        k = j
+    gp = np.zeros(len(counts) + 1, dtype=np.int64)
+    if counts:
+        np.cumsum(np.asarray(tris, dtype=np.int64), out=gp[1:])
+    gcount = np.asarray(counts, dtype=np.int64)
+    goff = np.zeros(len(counts), dtype=np.int64)
+    if len(counts) > 1:
+        np.cumsum(gcount[:-1], out=goff[1:])
+    return RenderContext(
+        prefix=draw_list.prefix_sums.astype(np.int64), item_mv=item_mv, item_mw=item_mw,
+        item_vtx_off=np.zeros(n, dtype=np.int64), item_idx_off=np.zeros(n, dtype=np.int64),
+        meshes=meshes, item_mesh=item_mesh, group_prefix=gp, group_item_off=goff,
+        group_item_count=gcount, group_items=np.asarray(flat, dtype=np.int64),
+        max_instances=max_inst)
+
+
+def _work_table(starts: np.ndarray, counts: np.ndarray, unit_ids: np.ndarray,
+                begin: int, end: int, chunk: int):
+    """Units (items or groups) intersected with [begin, end) of their global
+    space, split into chunks of ``chunk`` triangles."""
+    s = starts
+    e = starts + counts
+    lo = np.maximum(s, begin)
+    hi = np.minimum(e, end)
+    keep = hi > lo
+    lo_l = (lo - s)[keep]
+    hi_l = (hi - s)[keep]
+    ids = unit_ids[keep]
+    nch = (hi_l - lo_l + chunk - 1) // chunk
+    cp = np.zeros(len(ids) + 1, dtype=np.int64)
+    np.cumsum(nch, out=cp[1:])
+    return ids.astype(np.int64), lo_l.astype(np.int64), hi_l.astype(np.int64), cp
+
+
+class PreparedFrame:
+    """A frame whose descriptors are resident on the device; ``launch()``
+    enqueues clear + stages 1-3 without synchronising (CUDA-graph capturable
+    once the queues are large enough)."""
+
+    def __init__(self, draw_list: DrawList, camera, cfg: RasterConfig,
+                 ctx: RenderContext | None = None, *, device=None,
+                 work_range=None, use_filter=None, fresh_fb=True):
+        _lib = N.lib()
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
+        self.cfg = cfg
+        self.camera = camera
+        self.width = camera.internal_width
+        self.height = camera.internal_height
+        self.total = int(draw_list.total_triangles)
+        self.n_items = len(draw_list.items)
+        if ctx is None:
+            ctx = build_context(draw_list, camera)
+        self.ctx = ctx
+        self.instanced = (cfg.instancing == "on"
+                          or (cfg.instancing == "auto" and ctx.max_instances >= 2))
+        if use_filter is None:
+            use_filter = _FILTER_DEFAULT
+        self.use_filter = bool(use_filter) and cfg.force_stage < 2
+        self.geo = scene_geometry(ctx.meshes, device)
+        geo = self.geo
+        self.s2_cap = cfg.resolved_stage2_capacity(self.total)
+        self.s3_cap = cfg.resolved_stage3_capacity(self.total)
+        ws = workspace(device)
+        self.ws = ws
+        self.fb = ws.framebuffer(self.width * self.height, fresh_fb)
+
+        n = self.n_items
+        vtx_off = np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64)
+        idx_off = np.asarray([geo.idx_off[i] for i in ctx.item_mesh], dtype=np.int64)
+        p = projection_vector(camera)
+        p0, p1 = float(p[0]), float(p[1])
+        self.p0, self.p1 = p0, p1
+        pos_bound = np.stack([geo.meshes[i].pos_bound for i in ctx.item_mesh]) if n else \
+            np.zeros((0, 3))
+        qgrid = np.stack([geo.meshes[i].qgrid for i in ctx.item_mesh]) if n else np.zeros((0, 6))
+        pack = np.asarray([geo.meshes[i].pack for i in ctx.item_mesh], dtype=np.int64).reshape(n, 2)
+        filt = filter_rows(ctx.item_mv.reshape(n, 12), pos_bound, p0, p1, self.width,
+                           self.height, float(camera.near))
+        if geo.pos_format == N.POS_U16:
+            # the fp32 filter decodes with these rounded grid values; make the
+            # bound cover them: |gmin| + |gsize| already sized in pos_bound
+            pass
+
+        if work_range is None:
+            work_range = (0, int(ctx.group_prefix[-1]) if self.instanced else self.total)
+        self.work_range = (int(work_range[0]), int(work_range[1]))
+        chunk = int(_lib.curast_chunk_tris(int(self.instanced)))
+        if self.instanced:
+            ng = len(ctx.group_item_count)
+            tris = np.diff(ctx.group_prefix)
+            u = _work_table(ctx.group_prefix[:-1], tris, np.arange(ng), *self.work_range, chunk)
+        else:
+            counts = np.diff(ctx.prefix)
+            u = _work_table(ctx.prefix[:-1], counts, np.arange(n), *self.work_range, chunk)
+        self.unit_index, self.unit_lo, self.unit_hi, self.unit_cp = u
+
+        up = PackedUpload()
+        k_prefix = up.add(ctx.prefix)
+        k_mv = up.add(ctx.item_mv.reshape(-1))
+        k_mw = up.add(ctx.item_mw.reshape(-1))
+        k_vo = up.add(vtx_off)
+        k_io = up.add(idx_off)
+        k_f = up.add(filt.reshape(-1))
+        k_q = up.add(qgrid.reshape(-1).astype(np.float64))
+        k_pk = up.add(pack.reshape(-1))
+        k_gp = up.add(ctx.group_prefix)
+        k_go = up.add(ctx.group_item_off)
+        k_gc = up.add(ctx.group_item_count)
+        k_gi = up.add(ctx.group_items)
+        k_ui = up.add(self.unit_index)
+        k_ul = up.add(self.unit_lo)
+        k_uh = up.add(self.unit_hi)
+        k_uc = up.add(self.unit_cp)
+        up.upload(device)
+        self.upload = up
+        self.h2d_bytes = up.nbytes
+
+        f = N.CurastFrame()
+        f.pos_format = geo.pos_format
+        f.idx_format = geo.idx_format
+        f.positions = geo.positions.data_ptr()
+        f.indices = geo.indices.data_ptr()
+        f.n_items = n
+        f.prefix = up.ptr(k_prefix)
+        f.item_mv = up.ptr(k_mv)
+        f.item_mw = up.ptr(k_mw)
+        f.item_vtx_off = up.ptr(k_vo)
+        f.item_idx_off = up.ptr(k_io)
+        f.item_filter = up.ptr(k_f)
+        f.item_qgrid = up.ptr(k_q)
+        f.item_pack = up.ptr(k_pk)
+        f.instanced = int(self.instanced)
+        f.use_filter = int(self.use_filter)
+        f.n_groups = len(ctx.group_item_count)
+        f.group_prefix = up.ptr(k_gp)
+        f.group_item_off = up.ptr(k_go)
+        f.group_item_count = up.ptr(k_gc)
+        f.group_items = up.ptr(k_gi)
+        f.n_units = len(self.unit_index)
+        f.unit_index = up.ptr(k_ui)
+        f.unit_lo = up.ptr(k_ul)
+        f.unit_hi = up.ptr(k_uh)
+        f.unit_chunk_prefix = up.ptr(k_uc)
+        f.chunk_tris = chunk
+        f.p0, f.p1, f.near = p0, p1, float(camera.near)
+        f.width, f.height = self.width, self.height
+        view = np.asarray(camera.view_transform, dtype=np.float64)
+        rot_t = np.ascontiguousarray(view[:3, :3].T).reshape(-1)
+        for i in range(9):
+            f.rot_t[i] = float(rot_t[i])
+        for i in range(3):
+            f.cam[i] = float(np.asarray(camera.position, dtype=np.float64)[i])
+            f.view_r2[i] = float(view[2, i])
+        f.view_t2 = float(view[2, 3])
+        f.tiny_cull = int(bool(cfg.tiny_cull))
+        f.force_stage = int(cfg.force_stage)
+        f.small_max = int(cfg.small_max_px)
+        f.medium_max = int(cfg.medium_max_px)
+        f.tile_px = int(cfg.tile_px)
+        f.fb = self.fb.data_ptr()
+        f.counters = ws.counters.data_ptr()
+        self.frame = f
+        self._size_queues(DEVICE_Q2_INITIAL, DEVICE_Q3_INITIAL)
+
+    def _size_queues(self, want2: int, want3: int):
+        ws = self.ws
+        a2 = min(self.s2_cap, max(want2, ws.q2_alloc))
+        a3 = min(self.s3_cap, max(want3, ws.q3_alloc))
+        ws.ensure_q2(a2)
+        ws.ensure_q3(a3)
+        self.q2_alloc = max(0, min(self.s2_cap, ws.q2_alloc))
+        self.q3_alloc = max(0, min(self.s3_cap, ws.q3_alloc))
+        self.frame.q2 = ws.q2.data_ptr()
+        self.frame.q2_cap = self.q2_alloc
+        self.frame.q3 = ws.q3.data_ptr()
+        self.frame.q3_cap = self.q3_alloc
+
+    def launch(self, stream=None, events=None):
+        """Enqueue clear + stages 1-3 on ``stream`` (default: torch's current)."""
+        L = N.lib()
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        fp = ctypes.byref(self.frame)
+        if events:
+            events[0].record()
+        N.check(L.curast_frame_clear(fp, st), "frame_clear")
+        if events:
+            events[1].record()
+        N.check(L.curast_stage1(fp, st), "stage1")
+        if events:
+            events[2].record()
+        N.check(L.curast_stage2(fp, st), "stage2")
+        if events:
+            events[3].record()
+        N.check(L.curast_stage3(fp, st), "stage3")
+        if events:
+            events[4].record()
+
+    def read_counters(self) -> np.ndarray:
+        ws = self.ws
+        ws.counters_host.copy_(ws.counters, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return ws.counters_host.numpy().copy()
+
+    def run(self, timed=True) -> tuple[np.ndarray, list]:
+        """Run until the queues were large enough; returns (counters,
+        per-stage seconds).  Raises CapacityError like the reference."""
+        while True:
+            events = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if timed else None
+            self.launch(events=events)
+            c = self.read_counters()
+            n2, n3 = int(c[N.C_Q2]), int(c[N.C_Q3])
+            if n2 > self.s2_cap:
+                raise CapacityError(
+                    f"stage-2 queue overflow: {n2} entries forwarded, "
+                    f"capacity {self.s2_cap}; raise stage2_capacity to at least {n2}")
+            if n2 > self.q2_alloc:
+                self._size_queues(n2, self.q3_alloc)
+                continue
+            if n3 > self.s3_cap:
+                raise CapacityError(
+                    f"stage-3 queue overflow: {n3} tile entries, capacity "
+                    f"{self.s3_cap}; raise stage3_capacity to at least {n3}")
+            if n3 > self.q3_alloc:
+                self._size_queues(self.q2_alloc, n3)
+                continue
+            secs = [0.0] * 4
+            if timed:
+                secs = [events[i].elapsed_time(events[i + 1]) * 1e-3 for i in range(4)]
+            return c, secs
+
+    def stats(self, c: np.ndarray, secs) -> FrameStats:
+        s1 = c[N.C_S1:N.C_S1 + 8]
+        s2 = c[N.C_S2:N.C_S2 + 5]
+        st = FrameStats(total_triangles=self.total, items=self.n_items,
+                        instanced=self.instanced)
+        st.stage1 = Stage1Stats(rasterized=int(s1[0]), forwarded=int(s1[1]),
+                                culled_frustum=int(s1[2]), culled_offscreen=int(s1[3]),
+                                culled_tiny=int(s1[4]), culled_backface=int(s1[5]),
+                                culled_degenerate=int(s1[6]), fragments=int(s1[7]))
+        st.stage2 = Stage2Stats(direct=int(s2[0]), tiled=int(s2[1]), dropped=int(s2[2]),
+                                tiles=int(s2[4]), fragments=int(s2[3]))
+        st.stage3 = Stage3Stats(entries=int(c[N.C_Q3]), fragments=int(c[N.C_S3]))
+        st.merge_s, st.stage1_s, st.stage2_s, st.stage3_s = secs
+        st.exact_fallbacks = int(c[N.C_EXACT])
+        return st
+
+
+def render_draw_list(draw_list: DrawList, camera, cfg: RasterConfig | None = None,
+                     ctx: RenderContext | None = None, *, use_filter=None,
+                     work_range=None) -> tuple[Framebuffer, FrameStats]:
+    """Run the three stages over a prebuilt draw list (pipeline.py:207-365).
+
+    The returned Framebuffer keeps its words in HBM (``device_words``);
+    ``.words`` downloads them as the reference's host ``np.uint64`` array."""
+    cfg = cfg or RasterConfig()
+    width, height = camera.internal_width, camera.internal_height
+    total = draw_list.total_triangles
+    if total == 0:
+        st = FrameStats(total_triangles=0, items=len(draw_list.items))
+        return Framebuffer(width, height), st
+    frame = PreparedFrame(draw_list, camera, cfg, ctx, use_filter=use_filter,
+                          work_range=work_range)
+    c, secs = frame.run()
+    return Framebuffer(width, height, device_words=frame.fb), frame.stats(c, secs)
+
+
+def render_frame(scene, camera, cfg: RasterConfig | None = None
+                 ) -> tuple[Framebuffer, FrameStats]:
+    """Frustum-cull, assemble the draw list, run all three stages
+    (pipeline.py:368-372)."""
+    return render_draw_list(build_draw_list(scene, camera), camera, cfg)
+
+
+# ---------------------------------------------------------------------------
+# classification mirror (pipeline.py:379-418) — host debug helper
+
+STAGE1 = 1
+STAGE2_DIRECT = 2
+STAGE3_TILED = 3
+
+
+def clip_triangle_near_plane(view_verts, near: float) -> np.ndarray:
+    """Sutherland-Hodgman against z = -near (kernels.py:257-281)."""
+    v = np.asarray(view_verts, dtype=np.float64)
+    out = []
+    for i in range(3):
+        j = (i + 1) % 3
+        da = -v[i, 2] - near
+        db = -v[j, 2] - near
+        if da >= 0.0:
+            out.append(v[i].copy())
+        if (da >= 0.0) != (db >= 0.0):
+            u = da / (da - db)
+            out.append(v[i] + u * (v[j] - v[i]))
+    return np.asarray(out, dtype=np.float64).reshape(-1, 3)
+
+
+def classify_route(view_verts, camera, cfg: RasterConfig | None = None):
+    cfg = cfg or RasterConfig()
+    v = np.asarray(view_verts, dtype=np.float64)
+    width, height = camera.internal_width, camera.internal_height
+    p = projection_vector(camera)
+    depths = -v[:, 2]
+    if np.all(depths < camera.near):
+        return None, 0
+    near_cross = bool(np.any(depths < camera.near))
+    poly = clip_triangle_near_plane(v, camera.near) if near_cross else v
+    if len(poly) == 0:
+        return None, 0
+    d = np.maximum(-poly[:, 2], camera.near)
+    px = (poly[:, 0] * p[0] / d + 1.0) * 0.5 * width
+    py = (1.0 - poly[:, 1] * p[1] / d) * 0.5 * height
+    ix0 = max(int(np.floor(px.min())), 0)
+    ix1 = min(int(np.ceil(px.max())), width)
+    iy0 = max(int(np.floor(py.min())), 0)
+    iy1 = min(int(np.ceil(py.max())), height)
+    if ix0 >= ix1 or iy0 >= iy1:
+        return None, 0
+    area = (ix1 - ix0) * (iy1 - iy0)
+    if near_cross or area >= cfg.medium_max_px:
+        return STAGE3_TILED, area
+    if area >= cfg.small_max_px:
+        return STAGE2_DIRECT, area
+    return STAGE1, area

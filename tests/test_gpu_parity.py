@@ -1,0 +1,198 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden outputs and the C oracle, bit-exact on visibility words and stats."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import host as oh
+from paper_2604_21749_b200 import (CLEAR, Camera, CapacityError, RasterConfig, SceneNode,
+                                   build_draw_list, render_draw_list, render_frame)
+from paper_2604_21749_b200 import generators as gen
+from paper_2604_21749_b200.pipeline import PreparedFrame, build_context
+from scenes import (STAT_ORDER, golden_camera, golden_cfg, golden_names, golden_scene,
+                    identity_camera, load_golden, mesh_from_soup, pixel_triangle_scene,
+                    random_scene, stats_vector_from_frame, stats_vector_from_oracle)
+
+pytestmark = pytest.mark.gpu
+
+NAMES = [n for n in golden_names() if n != "classifier_unstaged"]
+
+
+def _render_with_golden_ctx(g, cfg, compressed=True, use_filter=None):
+    scene = golden_scene(g, compressed=compressed)
+    cam = golden_camera(g)
+    dl = build_draw_list(scene, cam)
+    assert np.array_equal(dl.prefix_sums.astype(np.int64), g["prefix"])
+    ctx = build_context(dl, cam)
+    ctx.item_mv = np.ascontiguousarray(g["item_mv"])      # the reference's own matrices
+    return render_draw_list(dl, cam, cfg, ctx=ctx, use_filter=use_filter)
+
+
+@pytest.mark.parametrize("use_filter", [True, False])
+@pytest.mark.parametrize("name", NAMES)
+def test_golden_words_and_stats(name, use_filter):
+    g = load_golden(name)
+    if int(g["total"]) == 0:
+        pytest.skip("empty")
+    cfg = golden_cfg(g)
+    fb, st = _render_with_golden_ctx(g, cfg, use_filter=use_filter)
+    words = fb.words
+    diff = np.nonzero(words != g["ref_words"])[0]
+    assert diff.size == 0, f"{name}: {diff.size} differing words, first {diff[:8]}"
+    got = stats_vector_from_frame(st)
+    want = g["stats"][:15]
+    bad = [(STAT_ORDER[i], int(got[i]), int(want[i])) for i in range(15) if got[i] != want[i]]
+    assert not bad, bad
+    assert st.instanced == bool(g["stats"][15])
+
+
+def test_compressed_geometry_decoded_in_kernel():
+    g = load_golden("compressed_sphere")
+    fb_c, st_c = _render_with_golden_ctx(g, RasterConfig(), compressed=True)
+    fb_u, st_u = _render_with_golden_ctx(g, RasterConfig(), compressed=False)
+    assert np.array_equal(fb_c.words, g["ref_words"])
+    assert np.array_equal(fb_u.words, g["ref_words"])
+
+
+def test_random_scenes_seed2024_vs_oracle():
+    """Criterion 1 (test_acceptance.py:49-69): 200 random scenes, GPU vs the
+    sequential oracle run on this host."""
+    rng = np.random.default_rng(2024)
+    mism = []
+    for k in range(200):
+        scene, cam = random_scene(rng)
+        ref, _, dl = oh.render_reference(scene, cam)
+        fb, st = render_frame(scene, cam, RasterConfig())
+        if not np.array_equal(fb.words, ref):
+            mism.append(k)
+    assert not mism, mism
+
+
+def _bbox_scene(xs, ys, cam):
+    return pixel_triangle_scene([(0.25, 0.25), (xs - 0.25, 0.25), (0.25, ys - 0.25)],
+                                [2.0] * 3, cam)
+
+
+def test_capacity_errors_report_requirement():
+    cam = identity_camera(width=256, height=128)
+    scene = _bbox_scene(64, 64, cam)
+    m = scene[0].mesh
+    m.positions = np.tile(m.positions, (3, 1))
+    m.indices = np.arange(9, dtype=np.uint32)
+    m.triangle_count = 3
+    with pytest.raises(CapacityError, match="at least 3"):
+        render_frame(scene, cam, RasterConfig(stage2_capacity=1))
+    scene = _bbox_scene(130, 70, cam)
+    with pytest.raises(CapacityError, match="at least 6"):
+        render_frame(scene, cam, RasterConfig(stage3_capacity=2))
+
+
+def test_queue_autogrow_keeps_output(monkeypatch):
+    """Device queues start small and grow when a frame needs more than
+    allocated but less than the reference capacity."""
+    from paper_2604_21749_b200 import device as dv
+    cam = identity_camera(width=256, height=128)
+    scene = _bbox_scene(130, 70, cam)
+    ref, _, _ = oh.render_reference(scene, cam)
+    ws = dv.workspace(__import__("torch").device("cuda", 0))
+    ws.q3 = None
+    ws.q3_alloc = 0
+    monkeypatch.setattr("paper_2604_21749_b200.pipeline.DEVICE_Q3_INITIAL", 1)
+    fb, st = render_frame(scene, cam, RasterConfig())
+    assert st.stage2.tiles == 6
+    assert np.array_equal(fb.words, ref)
+
+
+def test_tiny_cull_and_instancing_toggles_bit_identical():
+    mesh = gen.make_tessellated_quad(300)
+    cam = Camera.look_at((0.0, 0.0, 3.2), (0.0, 0.0, 0.0), width=96, height=96)
+    scene = [SceneNode(mesh=mesh, transforms=[np.eye(4)])]
+    fb_on, st_on = render_frame(scene, cam, RasterConfig(tiny_cull=True))
+    fb_off, st_off = render_frame(scene, cam, RasterConfig(tiny_cull=False))
+    assert st_on.stage1.culled_tiny / st_on.total_triangles >= 0.30
+    assert np.array_equal(fb_on.words, fb_off.words)
+    scene = gen.make_lantern_grid(10, 10, tris_per_mesh=10 ** 4, spacing=1.8)
+    cam = Camera.look_at((0.0, 14.0, 20.0), (0.0, 0.0, 0.0), width=320, height=240)
+    fi, si = render_frame(scene, cam, RasterConfig(instancing="on"))
+    ff, sf = render_frame(scene, cam, RasterConfig(instancing="off"))
+    assert si.instanced and not sf.instanced
+    assert np.array_equal(fi.words, ff.words)
+    ref, rst, _ = oh.render_reference(scene, cam)
+    assert np.array_equal(fi.words, ref)
+    assert np.array_equal(stats_vector_from_frame(si), stats_vector_from_oracle(rst))
+
+
+def test_depth_winner_and_tie_break():
+    cam = identity_camera()
+    pix = [(30.25, 30.25), (40.75, 30.25), (30.25, 40.75)]
+    scene = pixel_triangle_scene(pix, [2.0, 2.0, 2.0], cam)
+    dup = SceneNode(mesh=mesh_from_soup(scene[0].mesh.positions.copy()), transforms=[np.eye(4)])
+    scene.append(dup)
+    fb, _ = render_frame(scene, cam, RasterConfig())
+    covered = fb.words[fb.words != CLEAR]
+    assert covered.size and ((covered & np.uint64(0xFFFFFFFFF)) == 0).all()
+
+
+def _oracle_threads():
+    return max(1, min(32, len(os.sched_getaffinity(0))))
+
+
+def test_config_a_sphere_1m_1080p_bit_exact():
+    scene, cam = gen.config_a()
+    fb, st = render_frame(scene, cam, RasterConfig())
+    ref, rst, _ = oh.render_reference(scene, cam, workers=_oracle_threads())
+    assert np.array_equal(fb.words, ref)
+    assert np.array_equal(stats_vector_from_frame(st), stats_vector_from_oracle(rst))
+    assert st.stage1.forwarded == 0
+
+
+def test_config_c_mixed_sizes_bit_exact():
+    scene, cam = gen.config_c()
+    fb, st = render_frame(scene, cam, RasterConfig())
+    ref, rst, _ = oh.render_reference(scene, cam, workers=_oracle_threads(),
+                                      s3_cap=1 << 22)
+    assert np.array_equal(fb.words, ref)
+    assert np.array_equal(stats_vector_from_frame(st), stats_vector_from_oracle(rst))
+    assert st.stage2.direct > 0 and st.stage2.tiled > 0 and st.stage3.fragments > 0
+
+
+@pytest.mark.slow
+def test_config_b_grid_100m_4k_bit_exact_and_filter_sound():
+    scene, cam = gen.config_b()
+    dl = build_draw_list(scene, cam)
+    fb, st = render_draw_list(dl, cam, RasterConfig())
+    words = fb.words.copy()
+    ref, rst, _ = oh.render_reference(scene, cam, workers=_oracle_threads(), s2_cap=1 << 20,
+                                      s3_cap=1 << 20)
+    assert np.array_equal(words, ref)
+    assert np.array_equal(stats_vector_from_frame(st), stats_vector_from_oracle(rst))
+    # exact-only path gives the same words
+    fb2, st2 = render_draw_list(dl, cam, RasterConfig(), use_filter=False)
+    assert np.array_equal(fb2.words, ref)
+    assert st2.exact_fallbacks == dl.total_triangles
+
+
+def test_filter_bound_never_violated():
+    """Every vertex's fp32 projection lies within the filter's error bound of
+    the exact fp64 value (curast_filter_check), on scenes with wide depth and
+    magnitude ranges."""
+    import ctypes
+    import torch
+    from paper_2604_21749_b200 import _native as N
+    scenes = [gen.config_a(), gen.config_b(n=1500)]
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        scenes.append(random_scene(rng))
+    for scene, cam in scenes:
+        dl = build_draw_list(scene, cam)
+        if dl.total_triangles == 0:
+            continue
+        pf = PreparedFrame(dl, cam, RasterConfig())
+        out = torch.zeros(3, dtype=torch.int64, device="cuda")
+        N.check(N.lib().curast_filter_check(ctypes.byref(pf.frame), out.data_ptr(),
+                                            torch.cuda.current_stream().cuda_stream), "check")
+        checked, bad, worst = (int(v) for v in out.cpu())
+        assert bad == 0, (checked, bad, worst / 1e6)
+        assert worst < 1_000_000

@@ -1,0 +1,187 @@
+"""CPU tests: host logic, generators, packing, C-ABI exports (no GPU)."""
+
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2604_21749_b200 import (CLEAR, Camera, CapacityError, MAX_TRIANGLE_ID,
+                                   RasterConfig, SceneNode, build_draw_list, pack_fragment,
+                                   unpack_fragment)
+from paper_2604_21749_b200 import _native as N
+from paper_2604_21749_b200 import codec
+from paper_2604_21749_b200.generators import (grid_indices, make_sphere,
+                                              make_tessellated_quad, sphere_dims_for)
+from paper_2604_21749_b200.pipeline import _work_table, build_context, classify_route
+from oracle import host as oh
+from scenes import (ROOT, golden_camera, golden_names, golden_scene, load_golden,
+                    mesh_from_soup, random_scene, view_point_for_pixel, identity_camera)
+
+
+def test_pack_fragment_golden_words():
+    assert pack_fragment(1.0, 7) == np.uint64(0x7F00000000000007)
+    assert pack_fragment(1.0, 0) == np.uint64(0x7F00000000000000)
+    g = np.load(os.path.join(ROOT, "tests", "golden", "packing.npz"))
+    got = np.array([pack_fragment(float(d), int(i)) for d, i in zip(g["depths"], g["ids"])],
+                   dtype=np.uint64)
+    assert np.array_equal(got, g["words"])
+    d28, d, tid = unpack_fragment(got[0])
+    assert tid == int(g["ids"][0])
+    with pytest.raises(ValueError):
+        unpack_fragment(CLEAR)
+    with pytest.raises(ValueError):
+        pack_fragment(-1.0, 0)
+    with pytest.raises(ValueError):
+        pack_fragment(1.0, MAX_TRIANGLE_ID)
+
+
+def test_generators_identical_to_reference():
+    g = np.load(os.path.join(ROOT, "tests", "golden", "generators.npz"))
+    for key in g.files:
+        if key.startswith("sphere_") and key.endswith("_pos"):
+            _, r, s, _ = key.split("_")
+            m = make_sphere(int(r), int(s))
+            assert np.array_equal(m.positions, g[key]), key
+            assert np.array_equal(m.indices, g[key.replace("_pos", "_idx")]), key
+            assert np.array_equal(m.vertex_colors, g[key.replace("_pos", "_col")]), key
+        if key.startswith("quad_") and key.endswith("_pos"):
+            n = int(key.split("_")[1])
+            m = make_tessellated_quad(n)
+            assert np.array_equal(m.positions, g[key]), key
+            assert np.array_equal(m.indices, g[key.replace("_pos", "_idx")]), key
+            assert np.array_equal(m.uvs, g[key.replace("_pos", "_uv")]), key
+    dims = np.array([sphere_dims_for(t) for t in (10, 2000, 10 ** 6, 10 ** 8)])
+    assert np.array_equal(dims, g["sphere_dims"])
+
+
+def test_random_scene_matches_reference_generator():
+    rng = np.random.default_rng(2024)
+    for k in range(40):
+        scene, cam = random_scene(rng)
+        gd = load_golden(f"random2024_{k:03d}")
+        assert int(gd["n_nodes"]) == len(scene)
+        for i, node in enumerate(scene):
+            assert np.array_equal(node.mesh.positions, gd[f"node{i}_positions"])
+            assert np.array_equal(np.stack(node.transforms), gd[f"node{i}_transforms"])
+        assert np.array_equal(cam.view_transform, gd["cam_view"])
+
+
+@pytest.mark.parametrize("name", golden_names("random2024_0")[:10] + ["lantern_on", "classifier"])
+def test_product_draw_list_matches_reference(name):
+    g = load_golden(name)
+    scene = golden_scene(g)
+    cam = golden_camera(g)
+    dl = build_draw_list(scene, cam)
+    assert np.array_equal(dl.prefix_sums.astype(np.int64), g["prefix"])
+    if dl.total_triangles:
+        ctx = build_context(dl, cam)
+        assert np.array_equal(ctx.item_mw, g["item_mw"])
+        np.testing.assert_allclose(ctx.item_mv, g["item_mv"], rtol=1e-14, atol=1e-14)
+        assert np.array_equal(ctx.group_prefix, g["group_prefix"])
+        assert np.array_equal(ctx.group_items, g["group_items"])
+        assert ctx.max_instances == int(g["max_instances"])
+
+
+def test_draw_list_capacity_error():
+    mesh = mesh_from_soup([(0, 0, -2.0), (1, 0, -2.0), (0, 1, -2.0)])
+    mesh.triangle_count = MAX_TRIANGLE_ID
+    with pytest.raises(CapacityError):
+        build_draw_list([SceneNode(mesh=mesh, transforms=[np.eye(4)])], identity_camera())
+    with pytest.raises(ValueError):
+        build_draw_list([], identity_camera())
+
+
+def test_codec_roundtrip():
+    rng = np.random.default_rng(11)
+    idx = rng.integers(2500, 3001, 500, dtype=np.uint32)
+    idx[0], idx[1] = 2500, 3000
+    p = codec.compress_indices(idx)
+    assert p.bits_per_index == 9
+    assert np.array_equal(p.decode_all(), idx)
+    assert all(p.decode(i) == idx[i] for i in range(0, 500, 37))
+    for _ in range(200):
+        bits = int(rng.integers(1, 33))
+        lo = int(rng.integers(0, 2 ** 31))
+        span = min(2 ** bits - 1, 2 ** 32 - 1 - lo)
+        buf = rng.integers(lo, lo + span + 1, int(rng.integers(1, 40)), dtype=np.int64).astype(np.uint32)
+        assert np.array_equal(codec.compress_indices(buf).decode_all(), buf)
+    aabb = np.array([[-7.0, 3.0, -1.0], [9.0, 3.5, 200.0]])
+    pts = rng.uniform(aabb[0], aabb[1], (1000, 3))
+    q = codec.quantize_positions(pts, aabb)
+    assert (np.abs(q.dequantize_all() - pts) <= (aabb[1] - aabb[0]) / 131072.0 + 1e-12).all()
+    # oracle host decode agrees with the product codec
+    m = mesh_from_soup(pts[:9])
+    m.positions = q
+    assert np.array_equal(oh.mesh_positions_f64(m), q.dequantize_all())
+
+
+def test_work_table_covers_range_exactly():
+    starts = np.array([0, 10, 10, 25], dtype=np.int64)
+    counts = np.array([10, 0, 15, 7], dtype=np.int64)
+    ids, lo, hi, cp = _work_table(starts, counts, np.arange(4), 5, 30, 4)
+    covered = []
+    for u in range(len(ids)):
+        covered += list(range(starts[ids[u]] + lo[u], starts[ids[u]] + hi[u]))
+        assert cp[u + 1] - cp[u] == -(-(hi[u] - lo[u]) // 4)
+    assert covered == list(range(5, 30))
+
+
+def test_grid_indices_layout():
+    m = make_tessellated_quad(3)
+    assert np.array_equal(grid_indices(3), m.indices)
+
+
+def test_classify_route_mirror():
+    cam = identity_camera(width=256, height=128)
+    for xs, ys, want in [(8, 8, 1), (16, 16, 2), (64, 64, 3)]:
+        pts = [view_point_for_pixel(0.25, 0.25, 2.0, cam),
+               view_point_for_pixel(xs - 0.25, 0.25, 2.0, cam),
+               view_point_for_pixel(0.25, ys - 0.25, 2.0, cam)]
+        assert classify_route(np.asarray(pts), cam)[0] == want
+
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "curast.h")).read()
+    return sorted(set(re.findall(r"\b(curast_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_c_abi_library_exports_every_header_symbol():
+    path = N.LIB_PATH
+    if not os.path.exists(path):
+        pytest.skip("library not built")
+    lib = ctypes.CDLL(path)
+    names = _header_functions()
+    assert "curast_stage1" in names and "curast_resolve" in names
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(N.EXPORTED_SYMBOLS) == set(names)
+    assert lib.curast_abi_version() == N.ABI_VERSION
+
+
+@pytest.mark.parametrize("cname,pyname", [("curast_frame_t", "CurastFrame"),
+                                           ("curast_resolve_t", "CurastResolve")])
+def test_struct_layout_matches_header(tmp_path, cname, pyname):
+    """Compile a probe against include/curast.h and compare every field
+    offset and the struct size with the ctypes mirror."""
+    import subprocess
+    cls = getattr(N, pyname)
+    fields = [f[0] for f in cls._fields_]
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "curast.h"',
+             "int main(void){",
+             f'printf("size %zu\\n", sizeof({cname}));']
+    for fn in fields:
+        lines.append(f'printf("{fn} %zu\\n", offsetof({cname}, {fn}));')
+    lines.append("return 0;}")
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    got = dict(l.split() for l in out.strip().splitlines())
+    assert int(got["size"]) == ctypes.sizeof(cls)
+    for fn in fields:
+        assert int(got[fn]) == getattr(cls, fn).offset, fn
