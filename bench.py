@@ -218,6 +218,7 @@ def run_ours(args):
                        "width": pf.width, "height": pf.height,
                        "parallelism": f"sort-last x{world}" if world > 1 else "single",
                        "l2": "inputs 1.8 GB per GPU >> 126 MB L2 (no flush needed)",
+                       "stage1_variant": os.environ.get("CURAST_S1", "cull"),
                        "stage_ms": {"clear": clr_ms, "stage1": s1_ms, "stage2": s2_ms,
                                     "stage3": s3_ms},
                        "exact_fp64_fraction": st.exact_fallbacks / max(1, T_rank),

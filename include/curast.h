@@ -60,6 +60,7 @@ enum curast_counter {
     CURAST_C_CLAIM2 = 17,
     CURAST_C_CLAIM3 = 18,
     CURAST_C_EXACT = 19,      /* stage-1 triangles decided by the fp64 path     */
+    CURAST_C_QX = 20,         /* fp64 work-queue entries (counts past capacity) */
     CURAST_COUNTER_SLOTS = 32
 };
 
@@ -75,6 +76,10 @@ enum curast_error {
  *   [12] E_xy  [13] E_d  (absolute error bounds of the fp32 rows)
  *   [14] near_hi (d above which the near tests are decided)  [15] unused  */
 #define CURAST_FILTER_FLOATS 16
+
+/* fp64 work-queue entry: 6 int64 words (48 B) */
+#define CURAST_QX_WORDS 6
+#define CURAST_QX_TAG 5
 
 typedef struct curast_frame {
     /* ---- geometry (device pointers, read-only) ---- */
@@ -126,6 +131,12 @@ typedef struct curast_frame {
     int64_t q2_cap;
     int64_t *q3;                      /* int64[q3_cap][4]  (item, local, tx, ty) */
     int64_t q3_cap;
+    int64_t *qx;                      /* int64[qx_cap][CURAST_QX_WORDS]: the
+                                         stage-1 triangles the fp32 filter left
+                                         to the exact fp64 kernel; word 5 =
+                                         item << 40 | local, words 0-4 = the 9
+                                         fp32 positions (POS_F32 producer)     */
+    int64_t qx_cap;
     int64_t *counters;                /* int64[CURAST_COUNTER_SLOTS]          */
 } curast_frame_t;
 

@@ -18,9 +18,10 @@ POS_F64, POS_F32, POS_U16 = 0, 1, 2
 IDX_U32, IDX_PACKED = 0, 1
 
 C_Q2, C_Q3, C_S1, C_S2, C_S3 = 0, 1, 2, 10, 15
-C_CLAIM1, C_CLAIM2, C_CLAIM3, C_EXACT = 16, 17, 18, 19
+C_CLAIM1, C_CLAIM2, C_CLAIM3, C_EXACT, C_QX = 16, 17, 18, 19, 20
 COUNTER_SLOTS = 32
 FILTER_FLOATS = 16
+QX_WORDS = 6
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -47,7 +48,7 @@ class CurastFrame(ctypes.Structure):
         ("tiny_cull", _I32), ("force_stage", _I32),
         ("small_max", _I64), ("medium_max", _I64), ("tile_px", _I64),
         ("fb", _P), ("q2", _P), ("q2_cap", _I64), ("q3", _P), ("q3_cap", _I64),
-        ("counters", _P),
+        ("qx", _P), ("qx_cap", _I64), ("counters", _P),
     ]
 
 

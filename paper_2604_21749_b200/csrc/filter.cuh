@@ -29,6 +29,10 @@ namespace curast {
 
 enum { FILT_EXACT = 0 };
 
+// relative slack covering rcp.approx (1 ulp), the fp32 multiply and the
+// comparison arithmetic: 2^-20 (>= 4x the 2^-22.4 they need together)
+constexpr float kRelSlack = 9.5367431640625e-07f;
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -71,7 +75,7 @@ __device__ __forceinline__ int filter_tri(const FilterConsts &F, float ax, float
     float miny = fminf(py0, fminf(py1, py2)), maxy = fmaxf(py0, fmaxf(py1, py2));
     float Mx = fmaxf(fmaxf(fabsf(minx), fabsf(maxx)), fmaxf(fabsf(miny), fabsf(maxy)));
     float eps = __fmaf_rn(Mx, F.ed, F.exy) * rcp_approx(dmin) * 1.5f;
-    eps = __fmaf_rn(Mx, 1.9073486e-06f /* 2^-19 */, eps) + WH_slack;
+    eps = __fmaf_rn(Mx, kRelSlack, eps) + WH_slack;
     // NDC frustum test (kernels.py:85-89) in pixel space: nx < -1 <=> px < 0
     if (maxx + eps < 0.0f || minx - eps > W || miny - eps > H || maxy + eps < 0.0f)
         return CULL_FRUSTUM;

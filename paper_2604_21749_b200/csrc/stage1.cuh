@@ -1,0 +1,371 @@
+// stage1.cuh — the stage-1 hot path (kernels.py:49-202): one persistent
+// kernel in which every warp works independently (no block barriers).
+//
+//   * a warp claims 2048-triangle chunks of one draw item with one atomic
+//     (the dynamic work counter of PAPER.md:258 at warp granularity);
+//   * each lane takes 4 consecutive triangles per step: their 12 indices are
+//     three 128-bit loads and all 36 position loads are issued before any
+//     arithmetic (memory-level parallelism instead of occupancy);
+//   * the fp32 cull filter (filter.cuh error model) runs on packed f32x2 FMAs
+//     (FFMA2 / FMUL2 / FADD2, sm_100a): (X, Y) of a vertex in one instruction;
+//   * triangles the filter cannot decide are appended to a per-warp queue in
+//     shared memory with ballot/popc; whenever 32 are pending, the warp runs
+//     the bit-exact fp64 classification + raster (exact.cuh) on all 32 lanes
+//     while the triangles' geometry is still in L1/L2.
+#pragma once
+#include "exact.cuh"
+#include "filter.cuh"
+
+namespace curast {
+
+constexpr int W_THREADS = 256;
+constexpr int W_WARPS = W_THREADS / 32;
+constexpr int W_TPL = 4;                       // consecutive triangles per lane per step
+constexpr int W_STEP = 32 * W_TPL;             // triangles per warp step
+constexpr int W_CHUNK = 2048;                  // triangles per warp claim
+constexpr int W_QCAP = 32 + W_STEP;            // per-warp fp64 queue
+
+struct FilterPairs {
+    float2 cx, cy, cz, c3;   // (X, Y) rows, per input coordinate
+    float dx, dy, dz, d3;    // d row
+    float exy, ed, near_hi;
+};
+
+__device__ __forceinline__ void load_filter_pairs(FilterPairs &F, const float *__restrict__ p) {
+    const float4 *q = (const float4 *)p;
+    float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
+    F.cx = make_float2(a.x, b.x);
+    F.cy = make_float2(a.y, b.y);
+    F.cz = make_float2(a.z, b.z);
+    F.c3 = make_float2(a.w, b.w);
+    F.dx = c.x; F.dy = c.y; F.dz = c.z; F.d3 = c.w;
+    F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
+}
+
+// fp32 cull filter on one triangle with packed (x, y) arithmetic.  Same
+// decisions and bound as filter_tri (filter.cuh).
+__device__ __forceinline__ int filter_tri2(const FilterPairs &F, const float *vx, const float *vy,
+                                           const float *vz, float2 WH, float slack, bool tiny_cull) {
+    float2 P[3];
+    float D[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float2 t = __ffma2_rn(F.cx, make_float2(vx[k], vx[k]), F.c3);
+        t = __ffma2_rn(F.cy, make_float2(vy[k], vy[k]), t);
+        t = __ffma2_rn(F.cz, make_float2(vz[k], vz[k]), t);
+        D[k] = __fmaf_rn(F.dz, vz[k], __fmaf_rn(F.dy, vy[k], __fmaf_rn(F.dx, vx[k], F.d3)));
+        float r = rcp_approx(D[k]);
+        P[k] = __fmul2_rn(t, make_float2(r, r));
+    }
+    const float dmin = fminf(D[0], fminf(D[1], D[2]));
+    if (!(dmin > F.near_hi)) return FILT_EXACT;          // near-plane outcomes: exact
+    const float2 mn = make_float2(fminf(P[0].x, fminf(P[1].x, P[2].x)),
+                                  fminf(P[0].y, fminf(P[1].y, P[2].y)));
+    const float2 mx = make_float2(fmaxf(P[0].x, fmaxf(P[1].x, P[2].x)),
+                                  fmaxf(P[0].y, fmaxf(P[1].y, P[2].y)));
+    const float M = fmaxf(fmaxf(fabsf(mn.x), fabsf(mx.x)), fmaxf(fabsf(mn.y), fabsf(mx.y)));
+    float eps = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(dmin);
+    eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, slack));
+    const float2 e2 = make_float2(eps, eps);
+    const float2 lo = __fadd2_rn(mn, make_float2(-eps, -eps));   // min - eps
+    const float2 hi = __fadd2_rn(mx, e2);                       // max + eps
+    // NDC frustum (kernels.py:85-89): all px < 0 | all px > W | py likewise
+    const float2 lo_w = __fadd2_rn(lo, make_float2(-WH.x, -WH.y));
+    if (fminf(hi.x, hi.y) < 0.0f || fmaxf(lo_w.x, lo_w.y) > 0.0f) return CULL_FRUSTUM;
+    if (!tiny_cull) return FILT_EXACT;
+    const float2 mxl = __fadd2_rn(mx, make_float2(-eps, -eps));  // max - eps
+    const float2 mnh = __fadd2_rn(mn, __fadd2_rn(e2, make_float2(-WH.x, -WH.y)));  // min + eps - WH
+    const float2 ext = __fadd2_rn(mxl, make_float2(-mn.x - eps, -mn.y - eps));      // max-min-2eps
+    // provably not frustum-culled, not offscreen (kernels.py:98-108)
+    const bool decided = fminf(mxl.x, mxl.y) > 0.0f && fmaxf(mnh.x, mnh.y) < 0.0f &&
+                         fminf(ext.x, ext.y) > 0.0f;
+    // tiny (kernels.py:110-115): smallest sample centre >= min lies > max
+    const float2 h = __fadd2_rn(make_float2(ceilf(lo.x - 0.5f), ceilf(lo.y - 0.5f)),
+                                make_float2(0.5f, 0.5f));
+    if (decided && (h.x > hi.x || h.y > hi.y)) return CULL_TINY;
+    return FILT_EXACT;
+}
+
+// Scalar fp32 cull filter, same decisions and bound as filter_tri, with a
+// short path for triangles whose eps-expanded bbox lies strictly inside the
+// viewport (then neither frustum cull can apply).
+__device__ __forceinline__ int filter_fast(const FilterConsts &F, const float *vx, const float *vy,
+                                           const float *vz, float W, float H, float slack,
+                                           bool tiny_cull) {
+    float px[3], py[3], D[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        D[k] = frow(F.c + 8, vx[k], vy[k], vz[k]);
+        const float X = frow(F.c, vx[k], vy[k], vz[k]);
+        const float Y = frow(F.c + 4, vx[k], vy[k], vz[k]);
+        const float r = rcp_approx(D[k]);
+        px[k] = X * r;
+        py[k] = Y * r;
+    }
+    const float dmin = fminf(D[0], fminf(D[1], D[2]));
+    if (!(dmin > F.near_hi)) return FILT_EXACT;
+    const float minx = fminf(px[0], fminf(px[1], px[2])), maxx = fmaxf(px[0], fmaxf(px[1], px[2]));
+    const float miny = fminf(py[0], fminf(py[1], py[2])), maxy = fmaxf(py[0], fmaxf(py[1], py[2]));
+    const float M = fmaxf(fmaxf(fabsf(minx), fabsf(maxx)), fmaxf(fabsf(miny), fabsf(maxy)));
+    float eps = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(dmin);
+    eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, slack));
+    const float lox = minx - eps, loy = miny - eps, hix = maxx + eps, hiy = maxy + eps;
+    if (lox > 0.0f && loy > 0.0f && hix < W && hiy < H) {
+        if (!tiny_cull) return FILT_EXACT;
+        const float e2 = eps + eps;
+        const bool ext = (maxx - minx > e2) && (maxy - miny > e2);
+        const bool tx = ceilf(lox - 0.5f) + 0.5f > hix;
+        const bool ty = ceilf(loy - 0.5f) + 0.5f > hiy;
+        return (ext && (tx || ty)) ? CULL_TINY : FILT_EXACT;
+    }
+    if (hix < 0.0f || lox > W || loy > H || hiy < 0.0f) return CULL_FRUSTUM;
+    const bool not_frustum = (maxx - eps > 0.0f) && (minx + eps < W) && (miny + eps < H) &&
+                             (maxy - eps > 0.0f);
+    if (!not_frustum || !tiny_cull) return FILT_EXACT;
+    const float e2 = eps + eps;
+    if (!(maxx - minx > e2 && maxy - miny > e2)) return FILT_EXACT;
+    if (ceilf(lox - 0.5f) + 0.5f > hix || ceilf(loy - 0.5f) + 0.5f > hiy) return CULL_TINY;
+    return FILT_EXACT;
+}
+
+// filter_fast with the (X, Y) rows and (px, py) on packed f32x2 FFMA2/FMUL2.
+__device__ __forceinline__ int filter_fast2(const FilterPairs &F, const float *vx, const float *vy,
+                                            const float *vz, float W, float H, float slack,
+                                            bool tiny_cull) {
+    float px[3], py[3], D[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        D[k] = __fmaf_rn(F.dz, vz[k], __fmaf_rn(F.dy, vy[k], __fmaf_rn(F.dx, vx[k], F.d3)));
+        float2 t = __ffma2_rn(F.cx, make_float2(vx[k], vx[k]), F.c3);
+        t = __ffma2_rn(F.cy, make_float2(vy[k], vy[k]), t);
+        t = __ffma2_rn(F.cz, make_float2(vz[k], vz[k]), t);
+        const float r = rcp_approx(D[k]);
+        const float2 p = __fmul2_rn(t, make_float2(r, r));
+        px[k] = p.x;
+        py[k] = p.y;
+    }
+    const float dmin = fminf(D[0], fminf(D[1], D[2]));
+    if (!(dmin > F.near_hi)) return FILT_EXACT;
+    const float minx = fminf(px[0], fminf(px[1], px[2])), maxx = fmaxf(px[0], fmaxf(px[1], px[2]));
+    const float miny = fminf(py[0], fminf(py[1], py[2])), maxy = fmaxf(py[0], fmaxf(py[1], py[2]));
+    const float M = fmaxf(fmaxf(fabsf(minx), fabsf(maxx)), fmaxf(fabsf(miny), fabsf(maxy)));
+    float eps = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(dmin);
+    eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, slack));
+    const float lox = minx - eps, loy = miny - eps, hix = maxx + eps, hiy = maxy + eps;
+    if (lox > 0.0f && loy > 0.0f && hix < W && hiy < H) {
+        if (!tiny_cull) return FILT_EXACT;
+        const float e2 = eps + eps;
+        const bool ext = (maxx - minx > e2) && (maxy - miny > e2);
+        const bool tx = ceilf(lox - 0.5f) + 0.5f > hix;
+        const bool ty = ceilf(loy - 0.5f) + 0.5f > hiy;
+        return (ext && (tx || ty)) ? CULL_TINY : FILT_EXACT;
+    }
+    if (hix < 0.0f || lox > W || loy > H || hiy < 0.0f) return CULL_FRUSTUM;
+    const bool not_frustum = (maxx - eps > 0.0f) && (minx + eps < W) && (miny + eps < H) &&
+                             (maxy - eps > 0.0f);
+    if (!not_frustum || !tiny_cull) return FILT_EXACT;
+    const float e2 = eps + eps;
+    if (!(maxx - minx > e2 && maxy - miny > e2)) return FILT_EXACT;
+    if (ceilf(lox - 0.5f) + 0.5f > hix || ceilf(loy - 0.5f) + 0.5f > hiy) return CULL_TINY;
+    return FILT_EXACT;
+}
+
+// Stage-1 cull filter (split mode producer): every warp claims chunks and
+// appends the triangles it cannot decide to the global fp64 queue with one
+// atomic per 128 triangles (warp prefix sum).
+template <int PF, int IF, int MINB, bool PAIR>
+__global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_t f) {
+    const int lane = threadIdx.x & 31;
+    unsigned int n_frustum = 0, n_tiny = 0;
+    const float W = (float)f.width, H = (float)f.height;
+    const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
+    const bool tiny = f.tiny_cull != 0;
+    const int64_t total = __ldg(f.unit_chunk_prefix + f.n_units);
+
+    for (;;) {
+        long long c = 0, item = 0, lo = 0, hi = 0;
+        if (lane == 0) {
+            c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1), 1ull);
+            if (c < total) {
+                int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
+                item = __ldg(f.unit_index + u);
+                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * W_CHUNK;
+                hi = __ldg(f.unit_hi + u);
+                hi = lo + W_CHUNK < hi ? lo + W_CHUNK : hi;
+            }
+        }
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= total) break;
+        item = __shfl_sync(0xffffffffu, item, 0);
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        hi = __shfl_sync(0xffffffffu, hi, 0);
+
+        FilterConsts F;
+        FilterPairs FP;
+        if (PAIR) load_filter_pairs(FP, f.item_filter + CURAST_FILTER_FLOATS * item);
+        else load_filter(F, f.item_filter + CURAST_FILTER_FLOATS * item);
+        ItemGeo<PF, IF> G;
+        G.load(f, item);
+        const int n_chunk = (int)(hi - lo);
+        const uint32_t *ibase = G.idx + 3 * lo;
+        const int64_t tag = (item << 40) | lo;
+        for (int s0 = 0; s0 < n_chunk; s0 += W_STEP) {
+            const int o = s0 + W_TPL * lane;
+            const int nv = max(0, min(W_TPL, n_chunk - o));
+            uint32_t ix[3 * W_TPL];
+            const uint32_t *ip = ibase + 3 * o;
+            if (IF == CURAST_IDX_U32 && nv == W_TPL && ((uintptr_t)ip & 15) == 0) {
+                const uint4 *v = (const uint4 *)ip;
+                uint4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
+                ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w;
+                ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
+                ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 3 * W_TPL; ++k)
+                    ix[k] = (k < 3 * nv) ? G.index(3 * (lo + o) + k) : 0u;
+            }
+            float px[3 * W_TPL], py[3 * W_TPL], pz[3 * W_TPL];
+#pragma unroll
+            for (int k = 0; k < 3 * W_TPL; ++k) G.pos32(ix[k], px[k], py[k], pz[k]);
+            unsigned need = 0;
+#pragma unroll
+            for (int t = 0; t < W_TPL; ++t) {
+                if (t < nv) {
+                    const int code =
+                        PAIR ? filter_fast2(FP, px + 3 * t, py + 3 * t, pz + 3 * t, W, H, slack, tiny)
+                             : filter_fast(F, px + 3 * t, py + 3 * t, pz + 3 * t, W, H, slack, tiny);
+                    n_frustum += (code == CULL_FRUSTUM);
+                    n_tiny += (code == CULL_TINY);
+                    need |= (code == FILT_EXACT) ? (1u << t) : 0u;
+                }
+            }
+            // warp prefix sum of the per-lane counts -> one atomic per step
+            const int mine = __popc(need);
+            int incl = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
+            if (wtotal) {
+                unsigned long long base = 0;
+                if (lane == 31)
+                    base = atomicAdd((unsigned long long *)(f.counters + CURAST_C_QX),
+                                     (unsigned long long)wtotal);
+                base = __shfl_sync(0xffffffffu, base, 31);
+                int64_t slot = (int64_t)base + incl - mine;
+                while (need) {
+                    const int t = __ffs(need) - 1;
+                    need &= need - 1;
+                    if (slot < f.qx_cap) f.qx[CURAST_QX_WORDS * slot + CURAST_QX_TAG] = tag + o + t;
+                    ++slot;
+                }
+            }
+        }
+    }
+    unsigned long long cnt[2] = {n_frustum, n_tiny};
+    flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+    flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+}
+
+struct WarpQueue {
+    int64_t ent[W_QCAP];     // item << 40 | local
+};
+
+template <int PF, int IF>
+__device__ __forceinline__ void wq_run(const curast_frame_t &f, const WarpQueue &q, int from,
+                                       int n, unsigned long long *cnt) {
+    const int lane = threadIdx.x & 31;
+    if (lane < n) {
+        const int64_t e = q.ent[from + lane];
+        s1_exact_entry<PF, IF>(f, e >> 40, e & ((1ll << 40) - 1), cnt);
+    }
+    __syncwarp();
+}
+
+template <int PF, int IF, int MINB>
+__global__ void __launch_bounds__(W_THREADS, MINB) k_s1_warp(const curast_frame_t f) {
+    __shared__ WarpQueue s_q[W_WARPS];
+    const int lane = threadIdx.x & 31;
+    WarpQueue &q = s_q[threadIdx.x >> 5];
+    int qn = 0;
+    unsigned long long cnt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned int n_frustum = 0, n_tiny = 0;
+    const float2 WH = make_float2((float)f.width, (float)f.height);
+    const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
+    const bool tiny = f.tiny_cull != 0;
+    const int64_t total = __ldg(f.unit_chunk_prefix + f.n_units);
+
+    for (;;) {
+        long long c = 0, item = 0, lo = 0, hi = 0;
+        if (lane == 0) {
+            c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1), 1ull);
+            if (c < total) {
+                int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
+                item = __ldg(f.unit_index + u);
+                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * W_CHUNK;
+                hi = __ldg(f.unit_hi + u);
+                hi = lo + W_CHUNK < hi ? lo + W_CHUNK : hi;
+            }
+        }
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= total) break;
+        item = __shfl_sync(0xffffffffu, item, 0);
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        hi = __shfl_sync(0xffffffffu, hi, 0);
+
+        FilterPairs F;
+        load_filter_pairs(F, f.item_filter + CURAST_FILTER_FLOATS * item);
+        ItemGeo<PF, IF> G;
+        G.load(f, item);
+        const int n_chunk = (int)(hi - lo);
+        const uint32_t *ibase = G.idx + 3 * lo;
+        for (int s0 = 0; s0 < n_chunk; s0 += W_STEP) {
+            const int o = s0 + W_TPL * lane;             // chunk-relative first triangle
+            const int nv = max(0, min(W_TPL, n_chunk - o));
+            uint32_t ix[3 * W_TPL];
+            const uint32_t *ip = ibase + 3 * o;
+            if (IF == CURAST_IDX_U32 && nv == W_TPL && ((uintptr_t)ip & 15) == 0) {
+                const uint4 *v = (const uint4 *)ip;
+                uint4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
+                ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w;
+                ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
+                ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 3 * W_TPL; ++k)
+                    ix[k] = (k < 3 * nv) ? G.index(3 * (lo + o) + k) : 0u;
+            }
+            float px[3 * W_TPL], py[3 * W_TPL], pz[3 * W_TPL];
+#pragma unroll
+            for (int k = 0; k < 3 * W_TPL; ++k) G.pos32(ix[k], px[k], py[k], pz[k]);
+#pragma unroll
+            for (int t = 0; t < W_TPL; ++t) {
+                int code = FILT_EXACT;
+                if (t < nv) {
+                    code = filter_tri2(F, px + 3 * t, py + 3 * t, pz + 3 * t, WH, slack, tiny);
+                    n_frustum += (code == CULL_FRUSTUM);
+                    n_tiny += (code == CULL_TINY);
+                }
+                const bool need = t < nv && code == FILT_EXACT;
+                const unsigned b = __ballot_sync(0xffffffffu, need);
+                if (need) q.ent[qn + __popc(b & ((1u << lane) - 1u))] = (item << 40) | (lo + o + t);
+                qn += __popc(b);
+            }
+            __syncwarp();
+            while (qn >= 32) {
+                qn -= 32;
+                wq_run<PF, IF>(f, q, qn, 32, cnt);
+            }
+        }
+    }
+    if (qn > 0) wq_run<PF, IF>(f, q, 0, qn, cnt);
+    cnt[CULL_FRUSTUM] += n_frustum;
+    cnt[CULL_TINY] += n_tiny;
+    flush_stats(f.counters + CURAST_C_S1, cnt, 8);
+    flush_stats(f.counters + CURAST_C_EXACT, cnt + 8, 1);
+}
+
+}  // namespace curast

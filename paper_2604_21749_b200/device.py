@@ -245,6 +245,8 @@ class Workspace:
         self.q2_alloc = 0
         self.q3 = None
         self.q3_alloc = 0
+        self.qx = None
+        self.qx_alloc = 0
         self.counters = torch.zeros(N.COUNTER_SLOTS, dtype=torch.int64, device=device)
         self.counters_host = torch.zeros(N.COUNTER_SLOTS, dtype=torch.int64).pin_memory()
 
@@ -264,6 +266,13 @@ class Workspace:
             self.q2 = torch.empty(2 * n, dtype=torch.int64, device=self.device)
             self.q2_alloc = n
         return self.q2
+
+    def ensure_qx(self, n: int):
+        n = max(1, int(n))
+        if n > self.qx_alloc:
+            self.qx = torch.empty(N.QX_WORDS * n, dtype=torch.int64, device=self.device)
+            self.qx_alloc = n
+        return self.qx
 
     def ensure_q3(self, n: int):
         n = max(1, int(n))

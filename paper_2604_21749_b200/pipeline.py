@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .config import (DEVICE_Q2_INITIAL, DEVICE_Q3_INITIAL, FrameStats, RasterConfig,
+from .config import (DEVICE_Q2_INITIAL, DEVICE_Q3_INITIAL, DEVICE_QX_INITIAL, FrameStats, RasterConfig,
                      Stage1Stats, Stage2Stats, Stage3Stats)
 from .device import PackedUpload, filter_rows, scene_geometry, workspace
 from .scene import (CLEAR, CapacityError, DrawList, Framebuffer, build_draw_list,
@@ -252,10 +252,21 @@ class PreparedFrame:
         f.fb = self.fb.data_ptr()
         f.counters = ws.counters.data_ptr()
         self.frame = f
+        if self.instanced:
+            gc = ctx.group_item_count[self.unit_index] if len(self.unit_index) else np.zeros(0)
+            self.qx_need_max = int(((self.unit_hi - self.unit_lo) * gc).sum())
+        else:
+            self.qx_need_max = int((self.unit_hi - self.unit_lo).sum())
         self._size_queues(DEVICE_Q2_INITIAL, DEVICE_Q3_INITIAL)
 
-    def _size_queues(self, want2: int, want3: int):
+    def _size_queues(self, want2: int, want3: int, wantx: int = 0):
         ws = self.ws
+        ax = min(max(1, self.qx_need_max), max(wantx, min(DEVICE_QX_INITIAL, self.qx_need_max),
+                                                ws.qx_alloc))
+        ws.ensure_qx(ax)
+        self.qx_alloc = ws.qx_alloc
+        self.frame.qx = ws.qx.data_ptr()
+        self.frame.qx_cap = self.qx_alloc
         a2 = min(self.s2_cap, max(want2, ws.q2_alloc))
         a3 = min(self.s3_cap, max(want3, ws.q3_alloc))
         ws.ensure_q2(a2)
@@ -300,20 +311,24 @@ class PreparedFrame:
             events = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if timed else None
             self.launch(events=events)
             c = self.read_counters()
+            nx = int(c[N.C_QX])
+            if nx > self.qx_alloc:
+                self._size_queues(self.q2_alloc, self.q3_alloc, nx)
+                continue
             n2, n3 = int(c[N.C_Q2]), int(c[N.C_Q3])
             if n2 > self.s2_cap:
                 raise CapacityError(
                     f"stage-2 queue overflow: {n2} entries forwarded, "
                     f"capacity {self.s2_cap}; raise stage2_capacity to at least {n2}")
             if n2 > self.q2_alloc:
-                self._size_queues(n2, self.q3_alloc)
+                self._size_queues(n2, self.q3_alloc, self.qx_alloc)
                 continue
             if n3 > self.s3_cap:
                 raise CapacityError(
                     f"stage-3 queue overflow: {n3} tile entries, capacity "
                     f"{self.s3_cap}; raise stage3_capacity to at least {n3}")
             if n3 > self.q3_alloc:
-                self._size_queues(self.q2_alloc, n3)
+                self._size_queues(self.q2_alloc, n3, self.qx_alloc)
                 continue
             secs = [0.0] * 4
             if timed:
@@ -333,7 +348,7 @@ class PreparedFrame:
                                 tiles=int(s2[4]), fragments=int(s2[3]))
         st.stage3 = Stage3Stats(entries=int(c[N.C_Q3]), fragments=int(c[N.C_S3]))
         st.merge_s, st.stage1_s, st.stage2_s, st.stage3_s = secs
-        st.exact_fallbacks = int(c[N.C_EXACT])
+        st.exact_fallbacks = int(c[N.C_QX]) + int(c[N.C_EXACT])
         return st
 
 

@@ -201,5 +201,68 @@ def main():
     print("wrote", len(cases), "fixtures")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def main_resolve():
+    """Resolve-pass fixtures: reference resolve_frame / downsample outputs."""
+    trirast, conftest = _import_reference()
+    from trirast.config import RasterConfig, ShadingConfig
+    from trirast.pipeline import render_frame
+    from trirast.resolvepass import downsample, resolve_frame
+    from trirast.scenecore import Camera, SceneNode, build_draw_list
+    from trirast.scenedesc import (make_checker_texture, make_sphere, make_tessellated_quad,
+                                   sphere_dims_for, make_classifier_scene)
+
+    def save(name, scene, cam, shadings):
+        fb, _ = render_frame(scene, cam, RasterConfig(workers=1))
+        dl = build_draw_list(scene, cam)
+        out = {"words": fb.words, "cam_position": cam.position, "cam_view": cam.view_transform,
+               "cam_scalars": np.array([cam.fovy, cam.aspect, cam.near]),
+               "cam_ints": np.array([cam.image_width, cam.image_height, cam.supersampling]),
+               "n_nodes": np.array(len(scene))}
+        for i, node in enumerate(scene):
+            m = node.mesh
+            out[f"node{i}_positions"] = m.positions_f64()
+            out[f"node{i}_indices"] = m.indices_u32()
+            out[f"node{i}_aabb"] = m.aabb
+            out[f"node{i}_tricount"] = np.array(m.triangle_count)
+            out[f"node{i}_transforms"] = np.stack(node.transforms)
+            if m.vertex_colors is not None:
+                out[f"node{i}_colors"] = m.vertex_colors
+            if m.uvs is not None:
+                out[f"node{i}_uvs"] = m.uvs
+            if m.texture is not None:
+                out[f"node{i}_nlevels"] = np.array(len(m.texture.levels))
+                for k, lv in enumerate(m.texture.levels):
+                    out[f"node{i}_level{k}"] = lv
+        for k, sh in enumerate(shadings):
+            img, st = resolve_frame(fb, dl, cam, sh)
+            out[f"shading{k}"] = np.array(repr((sh.mode, sh.headlight, tuple(sh.background),
+                                                sh.mip_filter, tuple(sh.base_color))))
+            out[f"image{k}"] = img
+            out[f"rstats{k}"] = np.array([st.shaded, st.background, st.degenerate])
+            if cam.supersampling > 1:
+                out[f"down{k}"] = downsample(img, cam.supersampling)
+        np.savez_compressed(os.path.join(HERE, f"resolve_{name}.npz"), **out)
+
+    sph = make_sphere(*sphere_dims_for(20000))
+    cam = Camera.look_at((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), width=320, height=240)
+    save("sphere", [SceneNode(mesh=sph, transforms=[np.eye(4)])], cam,
+         [ShadingConfig(), ShadingConfig(headlight=True), ShadingConfig(mode="flat")])
+    scene, cam = make_classifier_scene()
+    save("classifier", scene, cam, [ShadingConfig(), ShadingConfig(headlight=True)])
+    quad = make_tessellated_quad(48)
+    quad.texture = make_checker_texture()
+    cam = Camera.look_at((0.3, -0.2, 1.4), (0, 0, 0), width=160, height=120, supersampling=2)
+    save("textured", [SceneNode(mesh=quad, transforms=[np.eye(4)])], cam,
+         [ShadingConfig(), ShadingConfig(mip_filter="trilinear", headlight=True)])
+    cam = Camera.look_at((0.0, 0.0, 4.5), (0, 0, 0), width=160, height=120, supersampling=4)
+    save("textured_far", [SceneNode(mesh=quad, transforms=[np.eye(4)])], cam,
+         [ShadingConfig(mip_filter="trilinear"), ShadingConfig()])
+    print("wrote resolve fixtures")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "resolve":
+    main_resolve()

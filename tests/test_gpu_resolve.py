@@ -1,0 +1,88 @@
+"""Resolve pass (K4) + downsample against the reference's resolve_frame
+outputs (tests/golden/resolve_*.npz).  Tolerance parity:
+background pixels exact, shaded channels within +-1 (the reference's BLAS /
+einsum summation order is unspecified), reference stats exact."""
+
+import ast
+
+import numpy as np
+import pytest
+
+from paper_2604_21749_b200 import Camera, Framebuffer, Mesh, SceneNode, ShadingConfig, build_draw_list
+from paper_2604_21749_b200.resolve import downsample, resolve_frame
+from scenes import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+class _Chain:
+    def __init__(self, levels):
+        self.levels = levels
+
+    @property
+    def base(self):
+        return self.levels[0]
+
+
+def _load(name):
+    g = dict(np.load(f"{GOLDEN}/resolve_{name}.npz"))
+    nodes = []
+    for i in range(int(g["n_nodes"])):
+        tex = None
+        if f"node{i}_nlevels" in g:
+            tex = _Chain([g[f"node{i}_level{k}"] for k in range(int(g[f"node{i}_nlevels"]))])
+        mesh = Mesh(positions=g[f"node{i}_positions"], indices=g[f"node{i}_indices"],
+                    triangle_count=int(g[f"node{i}_tricount"]), aabb=g[f"node{i}_aabb"],
+                    vertex_colors=g.get(f"node{i}_colors"), uvs=g.get(f"node{i}_uvs"),
+                    texture=tex)
+        nodes.append(SceneNode(mesh=mesh, transforms=list(g[f"node{i}_transforms"])))
+    fovy, aspect, near = (float(v) for v in g["cam_scalars"])
+    w, h, ss = (int(v) for v in g["cam_ints"])
+    cam = Camera(position=g["cam_position"], view_transform=g["cam_view"], fovy=fovy,
+                 aspect=aspect, near=near, image_width=w, image_height=h, supersampling=ss)
+    return g, nodes, cam
+
+
+@pytest.mark.parametrize("name", ["sphere", "classifier", "textured", "textured_far"])
+def test_resolve_matches_reference(name):
+    g, nodes, cam = _load(name)
+    dl = build_draw_list(nodes, cam)
+    fb = Framebuffer(cam.internal_width, cam.internal_height)
+    fb.words = g["words"]
+    k = 0
+    while f"image{k}" in g:
+        mode, headlight, bg, mip, base = ast.literal_eval(str(g[f"shading{k}"]))
+        sh = ShadingConfig(mode=mode, headlight=headlight, background=bg, mip_filter=mip,
+                           base_color=base)
+        img, st = resolve_frame(fb, dl, cam, sh)
+        ref = g[f"image{k}"]
+        bgmask = g["words"].reshape(ref.shape[:2]) == np.uint64(0xFFFFFFFFFFFFFFFF)
+        assert np.array_equal(img[bgmask], ref[bgmask])
+        diff = np.abs(img.astype(np.int16) - ref.astype(np.int16))
+        n_off = int((diff.max(axis=2) > 0).sum())
+        assert diff.max() <= 1, (name, k, int(diff.max()), n_off)
+        assert n_off <= max(10, 0.01 * (~bgmask).sum()), (name, k, n_off)
+        assert [st.shaded, st.background, st.degenerate] == list(g[f"rstats{k}"])
+        if f"down{k}" in g:
+            d = downsample(img, cam.supersampling)
+            dref = g[f"down{k}"]
+            assert np.abs(d.astype(np.int16) - dref.astype(np.int16)).max() <= 1
+            # exact on the reference's own image
+            assert np.array_equal(downsample(ref, cam.supersampling), dref)
+        k += 1
+
+
+def test_downsample_box_properties():
+    rng = np.random.default_rng(5)
+    for value in range(0, 256, 51):
+        img = np.full((8, 8, 4), value, dtype=np.uint8)
+        for f in (2, 4):
+            assert (downsample(img, f) == value).all()
+    for _ in range(20):
+        img = rng.integers(0, 256, (8, 8, 4), dtype=np.uint8)
+        for f in (2, 4):
+            out = downsample(img, f)
+            blocks = img.reshape(8 // f, f, 8 // f, f, 4).astype(np.uint32)
+            assert np.array_equal(out, (blocks.sum(axis=(1, 3)) // (f * f)).astype(np.uint8))
+    with pytest.raises(ValueError):
+        downsample(np.zeros((6, 8, 4), dtype=np.uint8), 4)
