@@ -46,16 +46,33 @@ class PackedIndexBuffer:
 
 
 def compress_indices(indices) -> PackedIndexBuffer:
-    idx = np.asarray(indices, dtype=np.uint32)
+    """Same bit stream as geomcodec.compress_indices (geomcodec.py:65-84),
+    built word-wise so 10^8-element buffers fit in memory: element i occupies
+    bits [i*b, i*b + b) of the little-endian 32-bit word stream, and since the
+    fields never overlap, OR-ing them equals summing them."""
+    idx = np.asarray(indices, dtype=np.uint32).ravel()
     if idx.size == 0:
         raise ValueError("indices must be non-empty")
     lo = int(idx.min())
     span = int(idx.max()) - lo
     b = max(1, span.bit_length())
-    rel = idx.astype(np.uint64) - np.uint64(lo)
-    bits = ((rel[:, None] >> np.arange(b, dtype=np.uint64)) & np.uint64(1)).astype(np.uint8)
-    return PackedIndexBuffer(min_index=lo, bits_per_index=b, count=idx.size,
-                             data=np.packbits(bits.ravel(), bitorder="little"))
+    n = idx.size
+    nbytes = (n * b + 7) // 8
+    nwords = (n * b + 31) // 32 + 1
+    words = np.zeros(nwords, dtype=np.uint64)
+    step = 1 << 24
+    for s in range(0, n, step):
+        rel = idx[s:s + step].astype(np.uint64) - np.uint64(lo)
+        bit = (np.arange(s, s + rel.size, dtype=np.uint64) * np.uint64(b))
+        w = (bit >> np.uint64(5)).astype(np.int64)
+        sh = bit & np.uint64(31)
+        full = rel << sh                                   # < 2^63
+        words += np.bincount(w, weights=(full & np.uint64(0xFFFFFFFF)).astype(np.float64),
+                             minlength=nwords).astype(np.uint64)
+        words += np.bincount(w + 1, weights=(full >> np.uint64(32)).astype(np.float64),
+                             minlength=nwords).astype(np.uint64)
+    data = words.astype(np.uint32).view(np.uint8)[:nbytes].copy()
+    return PackedIndexBuffer(min_index=lo, bits_per_index=b, count=n, data=data)
 
 
 @dataclass

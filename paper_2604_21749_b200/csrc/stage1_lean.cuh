@@ -112,9 +112,9 @@ __device__ __forceinline__ unsigned lean_bits(const LeanConsts &F, const float *
     return bits;
 }
 
-template <int PF, int MINB>
+template <int PF, int MINB, int TPL>
 __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f) {
-    constexpr int CHUNK = 2048, TPL = 4, STEP = 32 * TPL;
+    constexpr int CHUNK = 2048, STEP = 32 * TPL;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     unsigned n_frustum = 0, n_tiny = 0;
@@ -156,12 +156,16 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f) {
             const int o = s0 + TPL * lane;
             const int nv = max(0, min(TPL, n - o));
             uint32_t ix[3 * TPL];
-            if (vec && nv == TPL) {
+            if (TPL == 4 && vec && nv == TPL) {
                 const uint4 *v = (const uint4 *)(ib + 3 * o);
                 const uint4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
                 ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w;
                 ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
                 ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
+            } else if (TPL == 2 && vec && nv == TPL) {
+                const uint2 *v = (const uint2 *)(ib + 3 * o);
+                const uint2 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
+                ix[0] = a.x; ix[1] = a.y; ix[2] = b.x; ix[3] = b.y; ix[4] = d.x; ix[5] = d.y;
             } else {
 #pragma unroll
                 for (int k = 0; k < 3 * TPL; ++k) ix[k] = (k < 3 * nv) ? __ldg(ib + 3 * o + k) : 0u;
@@ -215,6 +219,90 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f) {
                 }
             }
         }
+    }
+    unsigned long long cnt[2] = {n_frustum, n_tiny};
+    flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+    flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+}
+
+// Instanced stage-1 filter (kernels.py:205-254): a lane owns one unique
+// triangle of a node group, fetches its indices and positions once and tests
+// it under every surviving instance transform of the group (the group is
+// uniform across the warp, so each instance's filter block is one broadcast
+// load).  Undecided (instance, triangle) pairs go to the fp64 queue with their
+// object-space positions; the exact kernel applies the instance's matrix.
+template <int PF, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) {
+    const int64_t CHUNK = f.chunk_tris;             // unique triangles per warp claim
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    unsigned n_frustum = 0, n_tiny = 0;
+    const float W = (float)f.width, H = (float)f.height;
+    const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
+    const bool tiny = f.tiny_cull != 0;
+    const int64_t total = __ldg(f.unit_chunk_prefix + f.n_units);
+    unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+
+    for (;;) {
+        long long c = 0, g = 0, lo = 0, hi = 0;
+        if (lane == 0) {
+            c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1), 1ull);
+            if (c < total) {
+                const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
+                g = __ldg(f.unit_index + u);
+                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * CHUNK;
+                hi = __ldg(f.unit_hi + u);
+                hi = lo + CHUNK < hi ? lo + CHUNK : hi;
+            }
+        }
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= total) break;
+        g = __shfl_sync(0xffffffffu, g, 0);
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        hi = __shfl_sync(0xffffffffu, hi, 0);
+        const int64_t ioff = __ldg(f.group_item_off + g);
+        const int64_t icount = __ldg(f.group_item_count + g);
+        const int64_t first = __ldg(f.group_items + ioff);
+        const float *pb = (const float *)f.positions + 3 * __ldg(f.item_vtx_off + first);
+        const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + first);
+      for (long long sub = lo; sub < hi; sub += 32) {
+        const int64_t local = sub + lane;
+        const bool valid = local < hi;
+        float x[3], y[3], z[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const uint32_t v = valid ? __ldg(ib + 3 * local + k) : 0u;
+            const float *p = pb + 3 * v;
+            x[k] = __ldg(p);
+            y[k] = __ldg(p + 1);
+            z[k] = __ldg(p + 2);
+        }
+        for (int64_t k = 0; k < icount; ++k) {
+            const int64_t item = __ldg(f.group_items + ioff + k);
+            LeanConsts F;
+            lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);
+            const unsigned bits = lean_bits(F, x, y, z, W, H, slack, tiny);
+            const bool need = valid && (bits & 1u);
+            if (valid && (bits & 2u)) ++n_frustum;
+            if (valid && bits == 0u) ++n_tiny;
+            const unsigned b = __ballot_sync(0xffffffffu, need);
+            if (b) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(qcount, (unsigned long long)__popc(b));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (need) {
+                    const long long slot = (long long)base + __popc(b & lt_mask);
+                    if (slot < f.qx_cap) {
+                        int64_t *e = f.qx + CURAST_QX_WORDS * slot;
+                        *(float4 *)e = make_float4(x[0], y[0], z[0], x[1]);
+                        *(float4 *)(e + 2) = make_float4(y[1], z[1], x[2], y[2]);
+                        *(float2 *)(e + 4) = make_float2(z[2], 0.0f);
+                        e[CURAST_QX_TAG] = (item << 40) | local;
+                    }
+                }
+            }
+        }
+      }
     }
     unsigned long long cnt[2] = {n_frustum, n_tiny};
     flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);

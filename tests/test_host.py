@@ -185,3 +185,22 @@ def test_struct_layout_matches_header(tmp_path, cname, pyname):
     assert int(got["size"]) == ctypes.sizeof(cls)
     for fn in fields:
         assert int(got[fn]) == getattr(cls, fn).offset, fn
+
+
+def test_compress_indices_matches_reference_bitstream():
+    g = load_golden("compressed_sphere")
+    mn, b, cnt = (int(v) for v in g["node0_p_meta"])
+    p = codec.compress_indices(g["node0_indices"])
+    assert (p.min_index, p.bits_per_index, p.count) == (mn, b, cnt)
+    assert np.array_equal(p.data, g["node0_p_data"])
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        bits = int(rng.integers(1, 33))
+        lo = int(rng.integers(0, 2 ** 31))
+        span = min(2 ** bits - 1, 2 ** 32 - 1 - lo)
+        buf = rng.integers(lo, lo + span + 1, int(rng.integers(1, 300)), dtype=np.int64).astype(np.uint32)
+        ref = np.packbits(((buf.astype(np.uint64)[:, None] - np.uint64(buf.min()))
+                           >> np.arange(max(1, int(buf.max() - buf.min()).bit_length()),
+                                        dtype=np.uint64) & np.uint64(1)).astype(np.uint8).ravel(),
+                          bitorder="little")
+        assert np.array_equal(codec.compress_indices(buf).data, ref)
