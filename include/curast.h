@@ -61,6 +61,7 @@ enum curast_counter {
     CURAST_C_CLAIM3 = 18,
     CURAST_C_EXACT = 19,      /* stage-1 triangles decided by the fp64 path     */
     CURAST_C_QX = 20,         /* fp64 work-queue entries (counts past capacity) */
+    CURAST_C_CLAIM1I = 21,    /* instanced-table claim counter (internal)       */
     CURAST_COUNTER_SLOTS = 32
 };
 
@@ -114,6 +115,16 @@ typedef struct curast_frame {
     const int64_t *unit_hi;
     const int64_t *unit_chunk_prefix; /* int64[n_units+1]                     */
     int64_t chunk_tris;               /* triangles per chunk (see curast_chunk_tris) */
+    /* second table for instanced frames: units = node groups with >= 2
+     * surviving instances (unique triangles x instances); single-instance
+     * groups go through the flat table above (same output, the flat kernel
+     * streams them faster)                                                 */
+    int64_t n_inst_units;
+    const int64_t *inst_unit_index;
+    const int64_t *inst_unit_lo;
+    const int64_t *inst_unit_hi;
+    const int64_t *inst_unit_chunk_prefix;
+    int64_t inst_chunk_tris;
     /* ---- camera (scenecore.py:119-127, pipeline.py:339-343) ---- */
     double p0, p1, near;
     int64_t width, height;

@@ -43,6 +43,8 @@ class CurastFrame(ctypes.Structure):
         ("group_item_count", _P), ("group_items", _P),
         ("n_units", _I64), ("unit_index", _P), ("unit_lo", _P), ("unit_hi", _P),
         ("unit_chunk_prefix", _P), ("chunk_tris", _I64),
+        ("n_inst_units", _I64), ("inst_unit_index", _P), ("inst_unit_lo", _P),
+        ("inst_unit_hi", _P), ("inst_unit_chunk_prefix", _P), ("inst_chunk_tris", _I64),
         ("p0", _D), ("p1", _D), ("near", _D), ("width", _I64), ("height", _I64),
         ("rot_t", _D * 9), ("cam", _D * 3), ("view_r2", _D * 3), ("view_t2", _D),
         ("tiny_cull", _I32), ("force_stage", _I32),

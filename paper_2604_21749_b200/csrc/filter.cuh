@@ -16,11 +16,12 @@
 // Error model (host computes E_xy, E_d per item, see device.py):
 //   X = px*d and Y = py*d are affine in the object position, d likewise.
 //   |X' - X| <= E_xy, |d' - d| <= E_d over the item's vertex box, with
-//   E = 16u * sum|coeff|*|pos| (u = 2^-24) covering coefficient rounding,
-//   the 3-FMA chain, and fp32 rounding/decode of the positions.
-//   |px' - px| <= 4/3 (E_xy + |px'| E_d) / d' + |px'| 2^-21 (rcp + mul)
+//   E = k u * sum|coeff|*|pos| (u = 2^-24; k = 6 / 7 / 10 for f32 / f64 /
+//   u16 positions) covering coefficient rounding, the 3-FMA chain, and fp32
+//   rounding/decode of the positions.
+//   |px' - px| <= 4/3 (E_xy + |px'| E_d) / d' + |px'| 1.5 * 2^-23 (rcp + mul)
 //   when d' > 4 E_d; fp64 rounding of the reference (<= 2^-50 relative) and
-//   the fp32 comparison arithmetic are covered by the 1.5x / 2^-19 / 2^-36
+//   the fp32 comparison arithmetic are covered by the 1.5x / 2^-21 / 2^-36
 //   slack terms.
 #pragma once
 #include "exact.cuh"
@@ -29,9 +30,10 @@ namespace curast {
 
 enum { FILT_EXACT = 0 };
 
-// relative slack covering rcp.approx (1 ulp), the fp32 multiply and the
-// comparison arithmetic: 2^-20 (>= 4x the 2^-22.4 they need together)
-constexpr float kRelSlack = 9.5367431640625e-07f;
+// relative slack on |px'|: rcp.approx (1 ulp = 2^-23), the fp32 multiply
+// (2^-24) and the comparison additions (2^-24 each) need < 1.5 * 2^-22;
+// 2^-21 keeps a 1.3x margin
+constexpr float kRelSlack = 4.76837158203125e-07f;
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;

@@ -233,25 +233,25 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f) {
 // object-space positions; the exact kernel applies the instance's matrix.
 template <int PF, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) {
-    const int64_t CHUNK = f.chunk_tris;             // unique triangles per warp claim
+    const int64_t CHUNK = f.inst_chunk_tris;             // unique triangles per warp claim
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     unsigned n_frustum = 0, n_tiny = 0;
     const float W = (float)f.width, H = (float)f.height;
     const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
     const bool tiny = f.tiny_cull != 0;
-    const int64_t total = __ldg(f.unit_chunk_prefix + f.n_units);
+    const int64_t total = __ldg(f.inst_unit_chunk_prefix + f.n_inst_units);
     unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
 
     for (;;) {
         long long c = 0, g = 0, lo = 0, hi = 0;
         if (lane == 0) {
-            c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1), 1ull);
+            c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1I), 1ull);
             if (c < total) {
-                const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
-                g = __ldg(f.unit_index + u);
-                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * CHUNK;
-                hi = __ldg(f.unit_hi + u);
+                const int64_t u = upper_index(f.inst_unit_chunk_prefix, f.n_inst_units + 1, c);
+                g = __ldg(f.inst_unit_index + u);
+                lo = __ldg(f.inst_unit_lo + u) + (c - __ldg(f.inst_unit_chunk_prefix + u)) * CHUNK;
+                hi = __ldg(f.inst_unit_hi + u);
                 hi = lo + CHUNK < hi ? lo + CHUNK : hi;
             }
         }

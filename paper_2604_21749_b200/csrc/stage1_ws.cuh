@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(WS_THREADS, 2) k_s1_ws(const curast_frame_t f)
                         if ((need >> t) & 1u) {
                             const unsigned T = base + __popc(b[t] & lt_mask);
                             const unsigned slot = T & (WS_RING - 1);
-                            while (vld(&s.freeq[slot]) != T) { }
+                            while (vld(&s.freeq[slot]) != T) __nanosleep(64);
                             WsEntry &e = s.ring[slot];
                             e.a = make_float4(px[3 * t], py[3 * t], pz[3 * t], px[3 * t + 1]);
                             e.b = make_float4(py[3 * t + 1], pz[3 * t + 1], px[3 * t + 2], py[3 * t + 2]);
@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(WS_THREADS, 2) k_s1_ws(const curast_frame_t f)
                 if (vld(&s.pub[slot]) == T + 1u) { have = true; break; }
                 const unsigned fin = vld(&s.final_tail);
                 if (fin != 0xFFFFFFFFu && T >= fin) break;
+                __nanosleep(256);     // idle consumers must not steal issue slots
             }
             if (have) {
                 __threadfence_block();

@@ -29,7 +29,11 @@ from . import _native as N
 from .codec import is_packed_indices, is_quantized_positions
 
 U = 2.0 ** -24
-E_FACTOR = 16.0
+# |X' - X| <= E_FACTOR * u * S per position format (S = sum |coeff * pos|):
+# coefficient rounding (1u) + the 3-FMA chain (3u) for exact f32 positions,
+# + 1u for f64 positions rounded to f32, + 3u for the u16 grid decode; the
+# factors below keep >= 1.2x margin over those sums.
+E_FACTOR = {N.POS_F32: 6.0, N.POS_F64: 7.0, N.POS_U16: 10.0}
 
 
 def _require_cuda():
@@ -189,7 +193,7 @@ def scene_geometry(meshes: list, device) -> SceneGeometry:
 
 # --------------------------------------------------------- filter constants
 def filter_rows(item_mv: np.ndarray, pos_bound: np.ndarray, p0: float, p1: float,
-                width: int, height: int, near: float) -> np.ndarray:
+                width: int, height: int, near: float, pos_format: int = N.POS_F64) -> np.ndarray:
     """fp32 filter block per item (curast.h CURAST_FILTER_FLOATS).
 
     X = px*d = A*vx + B*d, Y = py*d = Dh*d - C*vy, d = -vz with
@@ -208,8 +212,9 @@ def filter_rows(item_mv: np.ndarray, pos_bound: np.ndarray, p0: float, p1: float
     SX = ((np.abs(A * m[:, 0, :]) + np.abs(B * m[:, 2, :])) * P).sum(axis=1)
     SY = ((np.abs(C * m[:, 1, :]) + np.abs(Dh * m[:, 2, :])) * P).sum(axis=1)
     SD = (np.abs(m[:, 2, :]) * P).sum(axis=1)
-    exy = E_FACTOR * U * np.maximum(SX, SY) * (1 + 2.0 ** -20) + 1e-30
-    ed = E_FACTOR * U * SD * (1 + 2.0 ** -20) + 1e-30
+    ef = E_FACTOR[pos_format]
+    exy = ef * U * np.maximum(SX, SY) * (1 + 2.0 ** -20) + 1e-30
+    ed = ef * U * SD * (1 + 2.0 ** -20) + 1e-30
     near_hi = np.maximum(near + 2.0 * ed + 2.0 ** -40 * SD, 4.0 * ed)
     out = np.zeros((n, N.FILTER_FLOATS), dtype=np.float32)
     out[:, 0:4] = X

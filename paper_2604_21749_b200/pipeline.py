@@ -167,7 +167,7 @@ class PreparedFrame:
         qgrid = np.stack([geo.meshes[i].qgrid for i in ctx.item_mesh]) if n else np.zeros((0, 6))
         pack = np.asarray([geo.meshes[i].pack for i in ctx.item_mesh], dtype=np.int64).reshape(n, 2)
         filt = filter_rows(ctx.item_mv.reshape(n, 12), pos_bound, p0, p1, self.width,
-                           self.height, float(camera.near))
+                           self.height, float(camera.near), geo.pos_format)
         if geo.pos_format == N.POS_U16:
             # the fp32 filter decodes with these rounded grid values; make the
             # bound cover them: |gmin| + |gsize| already sized in pos_bound
@@ -176,15 +176,26 @@ class PreparedFrame:
         if work_range is None:
             work_range = (0, int(ctx.group_prefix[-1]) if self.instanced else self.total)
         self.work_range = (int(work_range[0]), int(work_range[1]))
-        chunk = int(_lib.curast_chunk_tris(int(self.instanced)))
+        chunk = int(_lib.curast_chunk_tris(0))
+        ichunk = int(_lib.curast_chunk_tris(1))
         if self.instanced:
+            # work space = unique triangles of the node groups (pipeline.py:244);
+            # single-instance groups stream through the flat kernel
             ng = len(ctx.group_item_count)
+            starts = ctx.group_prefix[:-1]
             tris = np.diff(ctx.group_prefix)
-            u = _work_table(ctx.group_prefix[:-1], tris, np.arange(ng), *self.work_range, chunk)
+            single = ctx.group_item_count == 1
+            first_item = ctx.group_items[ctx.group_item_off] if ng else np.zeros(0, np.int64)
+            u = _work_table(starts[single], tris[single], first_item[single],
+                            *self.work_range, chunk)
+            v = _work_table(starts[~single], tris[~single], np.arange(ng)[~single],
+                            *self.work_range, ichunk)
         else:
             counts = np.diff(ctx.prefix)
             u = _work_table(ctx.prefix[:-1], counts, np.arange(n), *self.work_range, chunk)
+            v = (np.zeros(0, np.int64),) * 3 + (np.zeros(1, np.int64),)
         self.unit_index, self.unit_lo, self.unit_hi, self.unit_cp = u
+        self.iunit_index, self.iunit_lo, self.iunit_hi, self.iunit_cp = v
 
         up = PackedUpload()
         k_prefix = up.add(ctx.prefix)
@@ -203,6 +214,10 @@ class PreparedFrame:
         k_ul = up.add(self.unit_lo)
         k_uh = up.add(self.unit_hi)
         k_uc = up.add(self.unit_cp)
+        k_vi = up.add(self.iunit_index)
+        k_vl = up.add(self.iunit_lo)
+        k_vh = up.add(self.iunit_hi)
+        k_vc = up.add(self.iunit_cp)
         up.upload(device)
         self.upload = up
         self.h2d_bytes = up.nbytes
@@ -234,6 +249,12 @@ class PreparedFrame:
         f.unit_hi = up.ptr(k_uh)
         f.unit_chunk_prefix = up.ptr(k_uc)
         f.chunk_tris = chunk
+        f.n_inst_units = len(self.iunit_index)
+        f.inst_unit_index = up.ptr(k_vi)
+        f.inst_unit_lo = up.ptr(k_vl)
+        f.inst_unit_hi = up.ptr(k_vh)
+        f.inst_unit_chunk_prefix = up.ptr(k_vc)
+        f.inst_chunk_tris = ichunk
         f.p0, f.p1, f.near = p0, p1, float(camera.near)
         f.width, f.height = self.width, self.height
         view = np.asarray(camera.view_transform, dtype=np.float64)
@@ -252,11 +273,9 @@ class PreparedFrame:
         f.fb = self.fb.data_ptr()
         f.counters = ws.counters.data_ptr()
         self.frame = f
-        if self.instanced:
-            gc = ctx.group_item_count[self.unit_index] if len(self.unit_index) else np.zeros(0)
-            self.qx_need_max = int(((self.unit_hi - self.unit_lo) * gc).sum())
-        else:
-            self.qx_need_max = int((self.unit_hi - self.unit_lo).sum())
+        gc = ctx.group_item_count[self.iunit_index] if len(self.iunit_index) else np.zeros(0)
+        self.qx_need_max = int((self.unit_hi - self.unit_lo).sum()
+                               + ((self.iunit_hi - self.iunit_lo) * gc).sum())
         self._size_queues(DEVICE_Q2_INITIAL, DEVICE_Q3_INITIAL)
 
     def _size_queues(self, want2: int, want3: int, wantx: int = 0):
