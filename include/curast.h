@@ -78,6 +78,10 @@ enum curast_error {
  *   [14] near_hi (d above which the near tests are decided)  [15] unused  */
 #define CURAST_FILTER_FLOATS 16
 
+/* instanced work units: inst_unit_index[u] = group | (first_instance << 32),
+ * covering instances [first, first + CURAST_INST_BLOCK) of the group */
+#define CURAST_INST_BLOCK 16
+
 /* fp64 work-queue entry: 6 int64 words (48 B) */
 #define CURAST_QX_WORDS 6
 #define CURAST_QX_TAG 5

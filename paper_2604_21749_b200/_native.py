@@ -21,6 +21,7 @@ C_Q2, C_Q3, C_S1, C_S2, C_S3 = 0, 1, 2, 10, 15
 C_CLAIM1, C_CLAIM2, C_CLAIM3, C_EXACT, C_QX = 16, 17, 18, 19, 20
 COUNTER_SLOTS = 32
 FILTER_FLOATS = 16
+INST_BLOCK = 16          # CURAST_INST_BLOCK: instances per instanced work unit
 QX_WORDS = 6
 
 _P = ctypes.c_void_p

@@ -260,8 +260,11 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) 
         g = __shfl_sync(0xffffffffu, g, 0);
         lo = __shfl_sync(0xffffffffu, lo, 0);
         hi = __shfl_sync(0xffffffffu, hi, 0);
+        // unit = group | first instance << 32 (CURAST_INST_BLOCK instances)
+        const int64_t k0 = g >> 32;
+        g &= 0xFFFFFFFFll;
         const int64_t ioff = __ldg(f.group_item_off + g);
-        const int64_t icount = __ldg(f.group_item_count + g);
+        const int64_t icount = min(__ldg(f.group_item_count + g), k0 + CURAST_INST_BLOCK);
         const int64_t first = __ldg(f.group_items + ioff);
         const float *pb = (const float *)f.positions + 3 * __ldg(f.item_vtx_off + first);
         const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + first);
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) 
             y[k] = __ldg(p + 1);
             z[k] = __ldg(p + 2);
         }
-        for (int64_t k = 0; k < icount; ++k) {
+        for (int64_t k = k0; k < icount; ++k) {
             const int64_t item = __ldg(f.group_items + ioff + k);
             LeanConsts F;
             lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);

@@ -32,6 +32,8 @@ from .device import PackedUpload, filter_rows, scene_geometry, workspace
 from .scene import (CLEAR, CapacityError, DrawList, Framebuffer, build_draw_list,
                     projection_vector)
 
+INST_BLOCK = N.INST_BLOCK
+
 # CURAST_FILTER=0 disables the fp32 cull filter (every triangle fp64) — a
 # debugging/verification switch, not a fallback.
 _FILTER_DEFAULT = os.environ.get("CURAST_FILTER", "1") != "0"
@@ -188,8 +190,14 @@ class PreparedFrame:
             first_item = ctx.group_items[ctx.group_item_off] if ng else np.zeros(0, np.int64)
             u = _work_table(starts[single], tris[single], first_item[single],
                             *self.work_range, chunk)
-            v = _work_table(starts[~single], tris[~single], np.arange(ng)[~single],
-                            *self.work_range, ichunk)
+            # multi-instance groups: one unit per block of CURAST_INST_BLOCK
+            # instances (unit id = group | first_instance << 32)
+            multi = np.nonzero(~single)[0]
+            nkb = -(-ctx.group_item_count[multi] // INST_BLOCK)
+            rep_g = np.repeat(multi, nkb)
+            kb = np.concatenate([np.arange(k) for k in nkb]) if len(nkb) else np.zeros(0, np.int64)
+            ids = rep_g.astype(np.int64) | ((kb.astype(np.int64) * INST_BLOCK) << 32)
+            v = _work_table(starts[rep_g], tris[rep_g], ids, *self.work_range, ichunk)
         else:
             counts = np.diff(ctx.prefix)
             u = _work_table(ctx.prefix[:-1], counts, np.arange(n), *self.work_range, chunk)
@@ -273,9 +281,14 @@ class PreparedFrame:
         f.fb = self.fb.data_ptr()
         f.counters = ws.counters.data_ptr()
         self.frame = f
-        gc = ctx.group_item_count[self.iunit_index] if len(self.iunit_index) else np.zeros(0)
+        if len(self.iunit_index):
+            k0 = self.iunit_index >> 32
+            gc = ctx.group_item_count[self.iunit_index & 0xFFFFFFFF]
+            per_unit = np.minimum(gc - k0, INST_BLOCK)
+        else:
+            per_unit = np.zeros(0, np.int64)
         self.qx_need_max = int((self.unit_hi - self.unit_lo).sum()
-                               + ((self.iunit_hi - self.iunit_lo) * gc).sum())
+                               + ((self.iunit_hi - self.iunit_lo) * per_unit).sum())
         self._size_queues(DEVICE_Q2_INITIAL, DEVICE_Q3_INITIAL)
 
     def _size_queues(self, want2: int, want3: int, wantx: int = 0):
