@@ -62,6 +62,8 @@ enum curast_counter {
     CURAST_C_EXACT = 19,      /* stage-1 triangles decided by the fp64 path     */
     CURAST_C_QX = 20,         /* fp64 work-queue entries (counts past capacity) */
     CURAST_C_CLAIM1I = 21,    /* instanced-table claim counter (internal)       */
+    CURAST_C_SLICE_CLAIM = 22,/* 4 slots: claim counters of stage-1 slices      */
+    CURAST_C_SLICE_SNAP = 26, /* 4 slots: fp64-queue size after each slice      */
     CURAST_COUNTER_SLOTS = 32
 };
 
@@ -119,6 +121,7 @@ typedef struct curast_frame {
     const int64_t *unit_hi;
     const int64_t *unit_chunk_prefix; /* int64[n_units+1]                     */
     int64_t chunk_tris;               /* triangles per chunk (see curast_chunk_tris) */
+    int64_t flat_chunks;              /* = unit_chunk_prefix[n_units] (host copy)  */
     /* second table for instanced frames: units = node groups with >= 2
      * surviving instances (unique triangles x instances); single-instance
      * groups go through the flat table above (same output, the flat kernel

@@ -43,7 +43,7 @@ class CurastFrame(ctypes.Structure):
         ("n_groups", _I64), ("group_prefix", _P), ("group_item_off", _P),
         ("group_item_count", _P), ("group_items", _P),
         ("n_units", _I64), ("unit_index", _P), ("unit_lo", _P), ("unit_hi", _P),
-        ("unit_chunk_prefix", _P), ("chunk_tris", _I64),
+        ("unit_chunk_prefix", _P), ("chunk_tris", _I64), ("flat_chunks", _I64),
         ("n_inst_units", _I64), ("inst_unit_index", _P), ("inst_unit_lo", _P),
         ("inst_unit_hi", _P), ("inst_unit_chunk_prefix", _P), ("inst_chunk_tris", _I64),
         ("p0", _D), ("p1", _D), ("near", _D), ("width", _I64), ("height", _I64),

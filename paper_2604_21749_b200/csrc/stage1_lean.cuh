@@ -113,7 +113,10 @@ __device__ __forceinline__ unsigned lean_bits(const LeanConsts &F, const float *
 }
 
 template <int PF, int MINB, int TPL>
-__global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f) {
+__global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f, int64_t cbeg,
+                                                        int64_t cend, int claim_slot) {
+    // processes chunks [cbeg, min(cend, total)) of the flat table, claimed
+    // through counters[claim_slot] (slices of one frame use distinct slots)
     constexpr int CHUNK = 2048, STEP = 32 * TPL;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -121,13 +124,13 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f) {
     const float W = (float)f.width, H = (float)f.height;
     const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
     const bool tiny = f.tiny_cull != 0;
-    const int64_t total = __ldg(f.unit_chunk_prefix + f.n_units);
+    const int64_t total = min(cend, __ldg(f.unit_chunk_prefix + f.n_units));
     unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
 
     for (;;) {
         long long c = 0, item = 0, lo = 0, hi = 0;
         if (lane == 0) {
-            c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1), 1ull);
+            c = cbeg + (long long)atomicAdd((unsigned long long *)(f.counters + claim_slot), 1ull);
             if (c < total) {
                 const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
                 item = __ldg(f.unit_index + u);

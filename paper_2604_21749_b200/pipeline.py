@@ -257,6 +257,7 @@ class PreparedFrame:
         f.unit_hi = up.ptr(k_uh)
         f.unit_chunk_prefix = up.ptr(k_uc)
         f.chunk_tris = chunk
+        f.flat_chunks = int(self.unit_cp[-1])
         f.n_inst_units = len(self.iunit_index)
         f.inst_unit_index = up.ptr(k_vi)
         f.inst_unit_lo = up.ptr(k_vl)
