@@ -1,17 +1,8 @@
-// stage1.cuh — the stage-1 hot path (kernels.py:49-202): one persistent
-// kernel in which every warp works independently (no block barriers).
-//
-//   * a warp claims 2048-triangle chunks of one draw item with one atomic
-//     (the dynamic work counter of PAPER.md:258 at warp granularity);
-//   * each lane takes 4 consecutive triangles per step: their 12 indices are
-//     three 128-bit loads and all 36 position loads are issued before any
-//     arithmetic (memory-level parallelism instead of occupancy);
-//   * the fp32 cull filter (filter.cuh error model) runs on packed f32x2 FMAs
-//     (FFMA2 / FMUL2 / FADD2, sm_100a): (X, Y) of a vertex in one instruction;
-//   * triangles the filter cannot decide are appended to a per-warp queue in
-//     shared memory with ballot/popc; whenever 32 are pending, the warp runs
-//     the bit-exact fp64 classification + raster (exact.cuh) on all 32 lanes
-//     while the triangles' geometry is still in L1/L2.
+// stage1.cuh — generic-format stage-1 cull filter (k_s1_cull): f64 / f32 /
+// u16 positions and u32 / bit-packed indices through ItemGeo, 4 consecutive
+// triangles per lane, warp-granular chunk claims, undecided triangles to the
+// fp64 queue with one atomic per 128 triangles.  The f32 + u32 layout uses
+// the leaner k_s1_lean (stage1_lean.cuh).
 #pragma once
 #include "exact.cuh"
 #include "filter.cuh"
@@ -268,104 +259,6 @@ __global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_
     unsigned long long cnt[2] = {n_frustum, n_tiny};
     flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
     flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
-}
-
-struct WarpQueue {
-    int64_t ent[W_QCAP];     // item << 40 | local
-};
-
-template <int PF, int IF>
-__device__ __forceinline__ void wq_run(const curast_frame_t &f, const WarpQueue &q, int from,
-                                       int n, unsigned long long *cnt) {
-    const int lane = threadIdx.x & 31;
-    if (lane < n) {
-        const int64_t e = q.ent[from + lane];
-        s1_exact_entry<PF, IF>(f, e >> 40, e & ((1ll << 40) - 1), cnt);
-    }
-    __syncwarp();
-}
-
-template <int PF, int IF, int MINB>
-__global__ void __launch_bounds__(W_THREADS, MINB) k_s1_warp(const curast_frame_t f) {
-    __shared__ WarpQueue s_q[W_WARPS];
-    const int lane = threadIdx.x & 31;
-    WarpQueue &q = s_q[threadIdx.x >> 5];
-    int qn = 0;
-    unsigned long long cnt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    unsigned int n_frustum = 0, n_tiny = 0;
-    const float2 WH = make_float2((float)f.width, (float)f.height);
-    const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
-    const bool tiny = f.tiny_cull != 0;
-    const int64_t total = __ldg(f.unit_chunk_prefix + f.n_units);
-
-    for (;;) {
-        long long c = 0, item = 0, lo = 0, hi = 0;
-        if (lane == 0) {
-            c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1), 1ull);
-            if (c < total) {
-                int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
-                item = __ldg(f.unit_index + u);
-                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * W_CHUNK;
-                hi = __ldg(f.unit_hi + u);
-                hi = lo + W_CHUNK < hi ? lo + W_CHUNK : hi;
-            }
-        }
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c >= total) break;
-        item = __shfl_sync(0xffffffffu, item, 0);
-        lo = __shfl_sync(0xffffffffu, lo, 0);
-        hi = __shfl_sync(0xffffffffu, hi, 0);
-
-        FilterPairs F;
-        load_filter_pairs(F, f.item_filter + CURAST_FILTER_FLOATS * item);
-        ItemGeo<PF, IF> G;
-        G.load(f, item);
-        const int n_chunk = (int)(hi - lo);
-        const uint32_t *ibase = G.idx + 3 * lo;
-        for (int s0 = 0; s0 < n_chunk; s0 += W_STEP) {
-            const int o = s0 + W_TPL * lane;             // chunk-relative first triangle
-            const int nv = max(0, min(W_TPL, n_chunk - o));
-            uint32_t ix[3 * W_TPL];
-            const uint32_t *ip = ibase + 3 * o;
-            if (IF == CURAST_IDX_U32 && nv == W_TPL && ((uintptr_t)ip & 15) == 0) {
-                const uint4 *v = (const uint4 *)ip;
-                uint4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
-                ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w;
-                ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
-                ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 3 * W_TPL; ++k)
-                    ix[k] = (k < 3 * nv) ? G.index(3 * (lo + o) + k) : 0u;
-            }
-            float px[3 * W_TPL], py[3 * W_TPL], pz[3 * W_TPL];
-#pragma unroll
-            for (int k = 0; k < 3 * W_TPL; ++k) G.pos32(ix[k], px[k], py[k], pz[k]);
-#pragma unroll
-            for (int t = 0; t < W_TPL; ++t) {
-                int code = FILT_EXACT;
-                if (t < nv) {
-                    code = filter_tri2(F, px + 3 * t, py + 3 * t, pz + 3 * t, WH, slack, tiny);
-                    n_frustum += (code == CULL_FRUSTUM);
-                    n_tiny += (code == CULL_TINY);
-                }
-                const bool need = t < nv && code == FILT_EXACT;
-                const unsigned b = __ballot_sync(0xffffffffu, need);
-                if (need) q.ent[qn + __popc(b & ((1u << lane) - 1u))] = (item << 40) | (lo + o + t);
-                qn += __popc(b);
-            }
-            __syncwarp();
-            while (qn >= 32) {
-                qn -= 32;
-                wq_run<PF, IF>(f, q, qn, 32, cnt);
-            }
-        }
-    }
-    if (qn > 0) wq_run<PF, IF>(f, q, 0, qn, cnt);
-    cnt[CULL_FRUSTUM] += n_frustum;
-    cnt[CULL_TINY] += n_tiny;
-    flush_stats(f.counters + CURAST_C_S1, cnt, 8);
-    flush_stats(f.counters + CURAST_C_EXACT, cnt + 8, 1);
 }
 
 }  // namespace curast
