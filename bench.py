@@ -273,9 +273,7 @@ def e2e_measure(dl, cam, cfg, total, world):
            "api": "paper_2604_21749_b200.render_draw_list + Framebuffer.words"}
     # cold: geometry upload inside the timed region (fresh device caches)
     mesh = dl.items[0].mesh
-    dv._mesh_cache.clear()
-    dv._mesh_cache_by_id.clear()
-    dv._scene_cache.clear()
+    dv.drop_device_copies([mesh])
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     fb, st = cr.render_draw_list(dl, cam, cfg)

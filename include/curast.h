@@ -40,7 +40,8 @@ extern "C" {
 
 enum curast_pos_format {
     CURAST_POS_F64 = 0,   /* double[V][3] (reference ctx.positions)            */
-    CURAST_POS_F32 = 1,   /* float[V][3], values exactly representable         */
+    CURAST_POS_F32 = 1,   /* float[V][4] (x, y, z, 0), values exactly f32: one
+                             128-bit load per vertex gather                    */
     CURAST_POS_U16 = 2    /* uint16[V][3] + per-item grid (geomcodec.py:87-101) */
 };
 enum curast_idx_format {

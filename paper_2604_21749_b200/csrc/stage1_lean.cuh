@@ -149,7 +149,9 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f, i
         lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);
         const int64_t vo = __ldg(f.item_vtx_off + item);
         const int64_t io = __ldg(f.item_idx_off + item);
-        const float *pb = (const float *)f.positions + 3 * vo;
+        // float4 positions: one 128-bit gather per vertex (the [V][3]
+        // layout cost 3 loads and ~3x the L1 wavefronts per warp gather)
+        const float4 *pb = (const float4 *)f.positions + vo;
         const uint32_t *ib = (const uint32_t *)f.indices + io + 3 * lo;
         const int n = (int)(hi - lo);
         const bool vec = (((uintptr_t)ib) & 15) == 0;
@@ -176,10 +178,10 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f, i
             float px[3 * TPL], py[3 * TPL], pz[3 * TPL];
 #pragma unroll
             for (int k = 0; k < 3 * TPL; ++k) {
-                const float *p = pb + 3 * ix[k];
-                px[k] = __ldg(p);
-                py[k] = __ldg(p + 1);
-                pz[k] = __ldg(p + 2);
+                const float4 q = __ldg(pb + ix[k]);
+                px[k] = q.x;
+                py[k] = q.y;
+                pz[k] = q.z;
             }
             unsigned need = 0, fr = 0;
 #pragma unroll
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) 
         const int64_t ioff = __ldg(f.group_item_off + g);
         const int64_t icount = min(__ldg(f.group_item_count + g), k0 + CURAST_INST_BLOCK);
         const int64_t first = __ldg(f.group_items + ioff);
-        const float *pb = (const float *)f.positions + 3 * __ldg(f.item_vtx_off + first);
+        const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + first);
         const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + first);
       for (long long sub = lo; sub < hi; sub += 32) {
         const int64_t local = sub + lane;
@@ -278,10 +280,10 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) 
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const uint32_t v = valid ? __ldg(ib + 3 * local + k) : 0u;
-            const float *p = pb + 3 * v;
-            x[k] = __ldg(p);
-            y[k] = __ldg(p + 1);
-            z[k] = __ldg(p + 2);
+            const float4 q = __ldg(pb + v);
+            x[k] = q.x;
+            y[k] = q.y;
+            z[k] = q.z;
         }
         for (int64_t k = k0; k < icount; ++k) {
             const int64_t item = __ldg(f.group_items + ioff + k);

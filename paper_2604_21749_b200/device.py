@@ -3,8 +3,9 @@
 Layout in HBM (per GPU):
 
 * geometry (uploaded once per mesh, cached on the mesh object's identity):
-  - positions: ``float32[V,3]`` when every coordinate is exactly
-    representable in float32 (12 B/vertex, the roofline layout);
+  - positions: ``float32[V,4]`` (x, y, z, 0) when every coordinate is
+    exactly representable in float32 (16 B/vertex: one 128-bit gather per
+    vertex, the roofline layout);
     ``float64[V,3]`` otherwise (the reference's ctx.positions);
     ``uint16[V,3]`` for ``QuantizedPositions`` (decoded in-register).
   - indices: ``uint32[3T]``, or the bit-packed stream of a
@@ -20,7 +21,6 @@ Layout in HBM (per GPU):
 from __future__ import annotations
 
 import math
-import weakref
 
 import numpy as np
 import torch
@@ -67,8 +67,12 @@ class DeviceMesh:
             self.qgrid = np.zeros(6)
             self.pos_bound = (np.abs(p64).max(axis=0) if len(p64) else np.zeros(3))
             if np.array_equal(p32.astype(np.float64), p64):
+                # float4 per vertex: a stage-1 vertex gather is one 128-bit
+                # load; the pad word is never read as data
                 self.pos_format = N.POS_F32
-                self.positions = torch.from_numpy(p32).to(device)
+                p4 = np.zeros((len(p32), 4), dtype=np.float32)
+                p4[:, :3] = p32
+                self.positions = torch.from_numpy(p4).to(device)
             else:
                 self.pos_format = N.POS_F64
                 self.positions = torch.from_numpy(p64).to(device)
@@ -92,7 +96,7 @@ class DeviceMesh:
             return self.positions
         if fmt == N.POS_F64:
             if self.pos_format == N.POS_F32:
-                return self.positions.double()
+                return self.positions[:, :3].double()
             q = self.positions.view(torch.int16).to(torch.int32) & 0xFFFF
             q = q.double()
             g = torch.from_numpy(self.qgrid).to(self.device)
@@ -115,26 +119,33 @@ class DeviceMesh:
         return (rel + mn).to(torch.int64).to(torch.int32)
 
 
-_mesh_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
-_mesh_cache_by_id: dict = {}
+_CACHE_ATTR = "_curast_device_copies"
 
 
 def device_mesh(mesh, device) -> DeviceMesh:
-    """Upload (once) and return the device copy of a mesh.  The cache entry is
-    keyed on the mesh object and validated against the identity of its
-    positions/indices objects, so replacing them re-uploads."""
-    key_objs = (id(mesh.positions), id(mesh.indices), int(mesh.triangle_count), str(device))
-    try:
-        ent = _mesh_cache.get(mesh)
-    except TypeError:
-        ent = _mesh_cache_by_id.get(id(mesh))
-    if ent is not None and ent[0] == key_objs:
-        return ent[1]
+    """Upload (once) and return the device copy of a mesh.
+
+    The copy is cached ON the mesh object (it dies with the mesh; an id-keyed
+    global table could hand a freed mesh's geometry to a new mesh that reuses
+    its id).  The entry holds the positions/indices objects it was built from
+    and is reused only while the mesh still holds those same objects, so
+    assigning new arrays re-uploads; in-place edits of the arrays are not
+    detected (assign a new array instead)."""
+    key = str(device)
+    cache = getattr(mesh, _CACHE_ATTR, None)
+    if cache is not None:
+        ent = cache.get(key)
+        if (ent is not None and ent[0] is mesh.positions and ent[1] is mesh.indices
+                and ent[2] == int(mesh.triangle_count)):
+            return ent[3]
     dm = DeviceMesh(mesh, device)
     try:
-        _mesh_cache[mesh] = (key_objs, dm)
-    except TypeError:
-        _mesh_cache_by_id[id(mesh)] = (key_objs, dm)
+        if cache is None:
+            cache = {}
+            object.__setattr__(mesh, _CACHE_ATTR, cache)
+        cache[key] = (mesh.positions, mesh.indices, int(mesh.triangle_count), dm)
+    except (AttributeError, TypeError):
+        pass                                    # slotted/frozen mesh: no cache
     return dm
 
 
@@ -164,7 +175,11 @@ class SceneGeometry:
             p = d.positions_as(self.pos_format)
             pos_parts.append(p.reshape(-1))
             ix = d.indices if self.idx_format == N.IDX_PACKED else d.indices_u32()
-            idx_parts.append(ix.reshape(-1))
+            ix = ix.reshape(-1)
+            if self.idx_format == N.IDX_U32 and ix.numel() % 4:
+                # keep every mesh's stream 16-byte aligned (128-bit index loads)
+                ix = torch.cat([ix, ix.new_zeros(4 - ix.numel() % 4)])
+            idx_parts.append(ix)
             nv += d.vertex_count
             ni += ix.numel()
         if len(dms) == 1:
@@ -180,15 +195,31 @@ _scene_cache: dict = {}
 
 
 def scene_geometry(meshes: list, device) -> SceneGeometry:
-    key = (tuple((id(m), id(m.positions), id(m.indices)) for m in meshes), str(device))
-    sg = _scene_cache.get(key)
-    if sg is not None:
-        return sg
-    if len(_scene_cache) > 8:
-        _scene_cache.clear()
+    """Cached concatenation for a draw list's unique meshes.  Entries hold the
+    mesh/positions/indices objects they were built from (so their ids cannot
+    be reused by new objects while the entry lives) and are matched by
+    identity; at most 8 scenes are kept."""
+    objs = tuple((m, m.positions, m.indices) for m in meshes)
+    key = (tuple(id(o) for t in objs for o in t), str(device))
+    ent = _scene_cache.get(key)
+    if ent is not None and all(a is b for ta, tb in zip(ent[0], objs) for a, b in zip(ta, tb)):
+        return ent[1]
+    if len(_scene_cache) >= 8:
+        _scene_cache.pop(next(iter(_scene_cache)))
     sg = SceneGeometry(meshes, device)
-    _scene_cache[key] = sg
+    _scene_cache[key] = (objs, sg)
     return sg
+
+
+def drop_device_copies(meshes=()) -> None:
+    """Forget cached device geometry (all scenes, and the given meshes' own
+    uploads) so the next frame re-uploads."""
+    _scene_cache.clear()
+    for m in meshes:
+        try:
+            delattr(m, _CACHE_ATTR)
+        except AttributeError:
+            pass
 
 
 # --------------------------------------------------------- filter constants

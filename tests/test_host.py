@@ -204,3 +204,38 @@ def test_compress_indices_matches_reference_bitstream():
                                         dtype=np.uint64) & np.uint64(1)).astype(np.uint8).ravel(),
                           bitorder="little")
         assert np.array_equal(codec.compress_indices(buf).data, ref)
+
+
+def test_device_copy_cache_is_identity_checked():
+    """Device geometry is cached on the mesh and matched by object identity:
+    a new mesh never inherits a freed mesh's upload (ids get reused), and
+    assigning new arrays re-uploads (device.py device_mesh/scene_geometry)."""
+    import gc
+
+    import torch
+
+    from paper_2604_21749_b200 import device as dv
+    from paper_2604_21749_b200.generators import make_sphere
+    cpu = torch.device("cpu")
+    m = make_sphere(4, 6)
+    m.positions = np.asarray(m.positions, np.float32).astype(np.float64)   # f32-exact
+    a = dv.device_mesh(m, cpu)
+    assert dv.device_mesh(m, cpu) is a
+    assert a.pos_format == N.POS_F32 and tuple(a.positions.shape) == (m.vertex_count(), 4)
+    assert torch.all(a.positions[:, 3] == 0)
+    sg = dv.scene_geometry([m], cpu)
+    assert dv.scene_geometry([m], cpu) is sg
+    m.positions = np.array(m.positions, copy=True) * 2.0
+    b = dv.device_mesh(m, cpu)
+    assert b is not a
+    assert np.array_equal(b.positions[:, :3].numpy(), np.asarray(m.positions, np.float32))
+    assert dv.scene_geometry([m], cpu) is not sg
+
+    for k in range(20):
+        mk = make_sphere(4 + k % 3, 6)
+        d = dv.scene_geometry([mk], cpu)
+        assert d.meshes[0].vertex_count == mk.vertex_count()
+        del mk, d
+        gc.collect()
+    dv.drop_device_copies([m])
+    assert dv.device_mesh(m, cpu) is not b
