@@ -65,6 +65,7 @@ enum curast_counter {
     CURAST_C_CLAIM1I = 21,    /* instanced-table claim counter (internal)       */
     CURAST_C_SLICE_CLAIM = 22,/* 4 slots: claim counters of stage-1 slices      */
     CURAST_C_SLICE_SNAP = 26, /* 4 slots: fp64-queue size after each slice      */
+    CURAST_C_PROVED = 30,     /* fp64-queue entries decided by the fp32 prover  */
     CURAST_COUNTER_SLOTS = 32
 };
 
@@ -85,6 +86,13 @@ enum curast_error {
  * covering instances [first, first + CURAST_INST_BLOCK) of the group */
 #define CURAST_INST_BLOCK 16
 
+/* meshlets: triangles per meshlet (a strip of 63 quads has 128 vertices),
+ * bytes per meshlet triangle record (3 u8 per triangle, padded), largest
+ * vertex list with u8 indices */
+#define CURAST_MESHLET_TRIS 126
+#define CURAST_MESHLET_BYTES 384
+#define CURAST_MESHLET_MAX_VERTS 256
+
 /* fp64 work-queue entry: 6 int64 words (48 B) */
 #define CURAST_QX_WORDS 6
 #define CURAST_QX_TAG 5
@@ -104,6 +112,16 @@ typedef struct curast_frame {
     const float *item_filter;         /* float[n_items][16] or NULL           */
     const double *item_qgrid;         /* U16: double[n_items][6] gmin, gsize  */
     const int64_t *item_pack;         /* PACKED: int64[n_items][2] min, bits  */
+    /* ---- meshlets of u32 index streams (optional: NULL = none) ----
+     * triangle t of a mesh lies in meshlet t / CURAST_MESHLET_TRIS; a meshlet
+     * lists its unique vertices (ascending mesh-local ids) and stores each
+     * triangle as 3 u8 indices into that list.  A meshlet with more than
+     * CURAST_MESHLET_MAX_VERTS vertices has no u8 form: its triangles are
+     * read from the index stream instead.                                  */
+    const int64_t *item_ml_off;       /* first meshlet of the item's mesh     */
+    const int64_t *ml_voff;           /* int64[n_meshlets+1] into ml_verts    */
+    const uint32_t *ml_verts;         /* mesh-local vertex ids                */
+    const uint8_t *ml_tris;           /* uint8[n_meshlets][CURAST_MESHLET_BYTES] */
     /* ---- instancing groups (pipeline.py:114-135) ---- */
     int32_t instanced;                /* 1: stage1_instanced_range semantics  */
     int32_t use_filter;               /* 1: fp32 cull filter + fp64 fallback  */

@@ -19,10 +19,14 @@ IDX_U32, IDX_PACKED = 0, 1
 
 C_Q2, C_Q3, C_S1, C_S2, C_S3 = 0, 1, 2, 10, 15
 C_CLAIM1, C_CLAIM2, C_CLAIM3, C_EXACT, C_QX = 16, 17, 18, 19, 20
+C_PROVED = 30
 COUNTER_SLOTS = 32
 FILTER_FLOATS = 16
 INST_BLOCK = 16          # CURAST_INST_BLOCK: instances per instanced work unit
 QX_WORDS = 6
+MESHLET_TRIS = 126       # CURAST_MESHLET_TRIS
+MESHLET_BYTES = 384      # CURAST_MESHLET_BYTES
+MESHLET_MAX_VERTS = 256  # CURAST_MESHLET_MAX_VERTS
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -39,6 +43,7 @@ class CurastFrame(ctypes.Structure):
         ("n_items", _I64), ("prefix", _P), ("item_mv", _P), ("item_mw", _P),
         ("item_vtx_off", _P), ("item_idx_off", _P), ("item_filter", _P),
         ("item_qgrid", _P), ("item_pack", _P),
+        ("item_ml_off", _P), ("ml_voff", _P), ("ml_verts", _P), ("ml_tris", _P),
         ("instanced", _I32), ("use_filter", _I32),
         ("n_groups", _I64), ("group_prefix", _P), ("group_item_off", _P),
         ("group_item_count", _P), ("group_items", _P),

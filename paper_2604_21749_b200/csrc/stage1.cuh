@@ -13,7 +13,7 @@ constexpr int W_THREADS = 256;
 constexpr int W_WARPS = W_THREADS / 32;
 constexpr int W_TPL = 4;                       // consecutive triangles per lane per step
 constexpr int W_STEP = 32 * W_TPL;             // triangles per warp step
-constexpr int W_CHUNK = 2048;                  // triangles per warp claim
+constexpr int W_CHUNK = kS1Chunk;              // triangles per warp claim
 constexpr int W_QCAP = 32 + W_STEP;            // per-warp fp64 queue
 
 struct FilterPairs {

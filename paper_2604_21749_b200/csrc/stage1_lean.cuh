@@ -18,48 +18,12 @@
 
 namespace curast {
 
-struct LeanConsts {
-    float2 cx, cy, cz, c3;   // (X, Y) rows
-    float dx, dy, dz, d3;    // d row
-    float exy, ed, near_hi;
-};
-
-__device__ __forceinline__ void lean_load(LeanConsts &F, const float *__restrict__ p) {
-    const float4 *q = (const float4 *)p;
-    const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
-    F.cx = make_float2(a.x, b.x);
-    F.cy = make_float2(a.y, b.y);
-    F.cz = make_float2(a.z, b.z);
-    F.c3 = make_float2(a.w, b.w);
-    F.dx = c.x; F.dy = c.y; F.dz = c.z; F.d3 = c.w;
-    F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
-}
-
-// 0 = fp64 needed, CULL_FRUSTUM, CULL_TINY
-__device__ __forceinline__ int lean_filter(const LeanConsts &F, const float *x, const float *y,
-                                           const float *z, float W, float H, float slack,
-                                           bool tiny) {
-    float2 P[3];
-    float D[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        D[k] = __fmaf_rn(F.dz, z[k], __fmaf_rn(F.dy, y[k], __fmaf_rn(F.dx, x[k], F.d3)));
-        float2 t = __ffma2_rn(F.cx, make_float2(x[k], x[k]), F.c3);
-        t = __ffma2_rn(F.cy, make_float2(y[k], y[k]), t);
-        t = __ffma2_rn(F.cz, make_float2(z[k], z[k]), t);
-        const float r = rcp_approx(D[k]);
-        P[k] = __fmul2_rn(t, make_float2(r, r));
-    }
-    const float dmin = fminf(D[0], fminf(D[1], D[2]));
-    const float mnx = fminf(P[0].x, fminf(P[1].x, P[2].x));
-    const float mxx = fmaxf(P[0].x, fmaxf(P[1].x, P[2].x));
-    const float mny = fminf(P[0].y, fminf(P[1].y, P[2].y));
-    const float mxy = fmaxf(P[0].y, fmaxf(P[1].y, P[2].y));
-    const float M = fmaxf(fmaxf(fabsf(mnx), fabsf(mxx)), fmaxf(fabsf(mny), fabsf(mxy)));
-    float eps = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(dmin);
-    eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, slack));
+// bit 0: needs fp64, bit 1: frustum-culled (else tiny-culled), from the fp32
+// bbox [mn, mx] of the projected vertices and its error bound eps
+__device__ __forceinline__ unsigned lean_decide(float mnx, float mxx, float mny, float mxy,
+                                                float eps, bool near_ok, float W, float H,
+                                                bool tiny) {
     const float lox = mnx - eps, loy = mny - eps, hix = mxx + eps, hiy = mxy + eps;
-    const bool near_ok = dmin > F.near_hi;
     // interior: neither frustum test can hold; offscreen then needs a
     // zero-extent bbox: hi - lo > 4 eps  <=>  max - min > 2 eps
     const bool interior = lox > 0.0f && loy > 0.0f && hix < W && hiy < H;
@@ -71,10 +35,12 @@ __device__ __forceinline__ int lean_filter(const LeanConsts &F, const float *x, 
     const bool is_tiny = near_ok && interior && tiny && ext && (tx || ty);
     // border / outside: only the frustum cull is decided here
     const bool is_fr = near_ok && !interior && (hix < 0.0f || hiy < 0.0f || lox > W || loy > H);
-    return is_tiny ? CULL_TINY : (is_fr ? CULL_FRUSTUM : FILT_EXACT);
+    unsigned bits = 0;
+    if (!(is_tiny || is_fr)) bits |= 1u;
+    if (is_fr) bits |= 2u;
+    return bits;
 }
 
-// bit 0: needs fp64, bit 1: frustum-culled (else tiny-culled)
 __device__ __forceinline__ unsigned lean_bits(const LeanConsts &F, const float *x, const float *y,
                                               const float *z, float W, float H, float slack,
                                               bool tiny) {
@@ -97,131 +63,375 @@ __device__ __forceinline__ unsigned lean_bits(const LeanConsts &F, const float *
     const float M = fmaxf(fmaxf(fabsf(mnx), fabsf(mxx)), fmaxf(fabsf(mny), fabsf(mxy)));
     float eps = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(dmin);
     eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, slack));
-    const float lox = mnx - eps, loy = mny - eps, hix = mxx + eps, hiy = mxy + eps;
-    const bool near_ok = dmin > F.near_hi;
-    const bool interior = lox > 0.0f && loy > 0.0f && hix < W && hiy < H;
-    const float e4 = 4.0f * eps;
-    const bool ext = (hix - lox > e4) && (hiy - loy > e4);
-    const bool tx = ceilf(lox - 0.5f) > hix - 0.5f;
-    const bool ty = ceilf(loy - 0.5f) > hiy - 0.5f;
-    const bool is_tiny = near_ok && interior && tiny && ext && (tx || ty);
-    const bool is_fr = near_ok && !interior && (hix < 0.0f || hiy < 0.0f || lox > W || loy > H);
-    unsigned bits = 0;
-    if (!(is_tiny || is_fr)) bits |= 1u;
-    if (is_fr) bits |= 2u;
-    return bits;
+    return lean_decide(mnx, mxx, mny, mxy, eps, dmin > F.near_hi, W, H, tiny);
 }
 
-template <int PF, int MINB, int TPL>
-__global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f, int64_t cbeg,
-                                                        int64_t cend, int claim_slot) {
-    // processes chunks [cbeg, min(cend, total)) of the flat table, claimed
-    // through counters[claim_slot] (slices of one frame use distinct slots)
-    constexpr int CHUNK = 2048, STEP = 32 * TPL;
-    const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned n_frustum = 0, n_tiny = 0;
-    const float W = (float)f.width, H = (float)f.height;
-    const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
-    const bool tiny = f.tiny_cull != 0;
-    const int64_t total = min(cend, __ldg(f.unit_chunk_prefix + f.n_units));
-    unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+// fp64 queue entry: the 9 object-space positions + tag (CURAST_QX_WORDS)
+__device__ __forceinline__ void qx_write(const curast_frame_t &f, long long slot, const float *x,
+                                         const float *y, const float *z, long long tag) {
+    if (slot >= f.qx_cap) return;
+    int64_t *e = f.qx + CURAST_QX_WORDS * slot;
+    *(float4 *)e = make_float4(x[0], y[0], z[0], x[1]);
+    *(float4 *)(e + 2) = make_float4(y[1], z[1], x[2], y[2]);
+    *(float2 *)(e + 4) = make_float2(z[2], 0.0f);
+    e[CURAST_QX_TAG] = tag;
+}
 
-    for (;;) {
-        long long c = 0, item = 0, lo = 0, hi = 0;
-        if (lane == 0) {
-            c = cbeg + (long long)atomicAdd((unsigned long long *)(f.counters + claim_slot), 1ull);
-            if (c < total) {
-                const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
-                item = __ldg(f.unit_index + u);
-                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * CHUNK;
-                hi = __ldg(f.unit_hi + u);
-                hi = lo + CHUNK < hi ? lo + CHUNK : hi;
+struct LeanCtx {
+    float W, H, slack;
+    bool tiny;
+    int lane;
+    unsigned lt_mask;
+    unsigned long long *qcount;
+};
+
+__device__ __forceinline__ LeanCtx lean_ctx(const curast_frame_t &f) {
+    LeanCtx C;
+    C.W = (float)f.width;
+    C.H = (float)f.height;
+    C.slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
+    C.tiny = f.tiny_cull != 0;
+    C.lane = threadIdx.x & 31;
+    C.lt_mask = (1u << C.lane) - 1u;
+    C.qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+    return C;
+}
+
+// Triangles [0, n) of an index range (ib = first triangle's indices, tag =
+// item << 40 | its local index): lane l owns TPL consecutive triangles per
+// 32*TPL step, 128-bit index loads when aligned, 3*TPL independent vertex
+// gathers issued before the math.  Warp-uniform n.
+// ILV: lane -> triangle map of a step.  0: lane l owns TPL consecutive
+// triangles (3 x 128-bit index loads); 1: lane l owns l, l+32, ... (scalar
+// index loads; each vertex gather of the warp then reads consecutive
+// triangles' vertices: fewer L1 lines per gather); 2: as 1, the indices
+// loaded as in 0 and transposed through shared memory (sidx: 32*3*TPL words
+// per warp).
+// PROBE (timing experiments only, wrong output): 1 = loads only.
+template <int TPL, int PROBE = 0, int ILV = 0>
+__device__ __forceinline__ void lean_range(const curast_frame_t &f, const LeanConsts &F,
+                                           const LeanCtx &C, const float4 *__restrict__ pb,
+                                           const uint32_t *__restrict__ ib, int n, long long tag,
+                                           unsigned &n_frustum, unsigned &n_tiny,
+                                           uint32_t *sidx = nullptr) {
+    constexpr int STEP = 32 * TPL;
+    constexpr int DT = ILV ? 32 : 1;
+    const bool vec = (((uintptr_t)ib) & 15) == 0;
+    for (int s0 = 0; s0 < n; s0 += STEP) {
+        const int o = ILV ? s0 + C.lane : s0 + TPL * C.lane;
+        unsigned valid;
+        if (ILV) {
+            valid = 0;
+#pragma unroll
+            for (int t = 0; t < TPL; ++t) valid |= (unsigned)(o + DT * t < n) << t;
+        } else {
+            const int nv = max(0, min(TPL, n - o));
+            valid = (1u << nv) - 1u;
+        }
+        uint32_t ix[3 * TPL];
+        if (ILV == 2 && TPL == 4 && vec && s0 + STEP <= n) {
+            const uint4 *v = (const uint4 *)(ib + 3 * s0) + 3 * C.lane;
+            uint4 *w = (uint4 *)sidx + 3 * C.lane;
+            w[0] = __ldg(v);
+            w[1] = __ldg(v + 1);
+            w[2] = __ldg(v + 2);
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < TPL; ++t)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) ix[3 * t + k] = sidx[3 * (C.lane + 32 * t) + k];
+            __syncwarp();
+        } else if (ILV == 0 && TPL == 4 && vec && valid == 15u) {
+            const uint4 *v = (const uint4 *)(ib + 3 * o);
+            const uint4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
+            ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w;
+            ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
+            ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
+        } else if (ILV == 0) {
+            const int lim = 3 * __popc(valid);
+#pragma unroll
+            for (int k = 0; k < 3 * TPL; ++k) ix[k] = k < lim ? __ldg(ib + 3 * o + k) : 0u;
+        } else {
+#pragma unroll
+            for (int t = 0; t < TPL; ++t)
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    ix[3 * t + k] = ((valid >> t) & 1u) ? __ldg(ib + 3 * (o + DT * t) + k) : 0u;
+        }
+        float px[3 * TPL], py[3 * TPL], pz[3 * TPL];
+#pragma unroll
+        for (int k = 0; k < 3 * TPL; ++k) {
+            const float4 q = __ldg(pb + ix[k]);
+            px[k] = q.x;
+            py[k] = q.y;
+            pz[k] = q.z;
+        }
+        if (PROBE == 1) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 3 * TPL; ++k) acc += px[k] + py[k] + pz[k];
+            n_tiny += acc == 12345.0f;
+            continue;
+        }
+        unsigned need = 0, fr = 0;
+#pragma unroll
+        for (int t = 0; t < TPL; ++t) {
+            const unsigned bits = lean_bits(F, px + 3 * t, py + 3 * t, pz + 3 * t, C.W, C.H, C.slack, C.tiny);
+            if ((valid >> t) & 1u) {
+                need |= (bits & 1u) << t;
+                fr |= (bits >> 1) << t;
             }
         }
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c >= total) break;
-        item = __shfl_sync(0xffffffffu, item, 0);
-        lo = __shfl_sync(0xffffffffu, lo, 0);
-        hi = __shfl_sync(0xffffffffu, hi, 0);
+        n_frustum += __popc(fr);
+        n_tiny += __popc(valid) - __popc(need) - __popc(fr);
+        unsigned b[TPL];
+        int tot = 0;
+#pragma unroll
+        for (int t = 0; t < TPL; ++t) {
+            b[t] = __ballot_sync(0xffffffffu, (need >> t) & 1u);
+            tot += __popc(b[t]);
+        }
+        if (tot) {
+            unsigned long long base = 0;
+            if (C.lane == 0) base = atomicAdd(C.qcount, (unsigned long long)tot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+            for (int t = 0; t < TPL; ++t) {
+                // positions travel with the entry: the fp64 kernel does not
+                // re-gather them from HBM
+                if ((need >> t) & 1u)
+                    qx_write(f, (long long)base + __popc(b[t] & C.lt_mask), px + 3 * t, py + 3 * t,
+                             pz + 3 * t, tag + o + DT * t);
+                base += __popc(b[t]);
+            }
+        }
+    }
+}
 
+// claims chunk c of the flat table through counters[claim_slot]; -1 when done
+__device__ __forceinline__ bool lean_claim(const curast_frame_t &f, int lane, int64_t cbeg,
+                                           int64_t total, int claim_slot, long long &item,
+                                           long long &lo, long long &hi) {
+    constexpr int CHUNK = kS1Chunk;
+    long long c = 0;
+    if (lane == 0) {
+        c = cbeg + (long long)atomicAdd((unsigned long long *)(f.counters + claim_slot), 1ull);
+        if (c < total) {
+            const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
+            item = __ldg(f.unit_index + u);
+            lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * CHUNK;
+            hi = __ldg(f.unit_hi + u);
+            hi = lo + CHUNK < hi ? lo + CHUNK : hi;
+        }
+    }
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= total) return false;
+    item = __shfl_sync(0xffffffffu, item, 0);
+    lo = __shfl_sync(0xffffffffu, lo, 0);
+    hi = __shfl_sync(0xffffffffu, hi, 0);
+    return true;
+}
+
+// Per-triangle lean kernel over the flat table: chunks [cbeg, min(cend,
+// total)) claimed through counters[claim_slot] (slices of one frame use
+// distinct slots).
+template <int PF, int MINB, int TPL, int PROBE = 0, int ILV = 0>
+__global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f, int64_t cbeg,
+                                                        int64_t cend, int claim_slot) {
+    __shared__ uint32_t sidx[ILV == 2 ? 8 : 1][ILV == 2 ? 3 * 32 * TPL : 1];
+    const LeanCtx C = lean_ctx(f);
+    unsigned n_frustum = 0, n_tiny = 0;
+    const int64_t total = min(cend, __ldg(f.unit_chunk_prefix + f.n_units));
+    for (;;) {
+        long long item = 0, lo = 0, hi = 0;
+        if (!lean_claim(f, C.lane, cbeg, total, claim_slot, item, lo, hi)) break;
         LeanConsts F;
         lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);
-        const int64_t vo = __ldg(f.item_vtx_off + item);
-        const int64_t io = __ldg(f.item_idx_off + item);
-        // float4 positions: one 128-bit gather per vertex (the [V][3]
-        // layout cost 3 loads and ~3x the L1 wavefronts per warp gather)
-        const float4 *pb = (const float4 *)f.positions + vo;
-        const uint32_t *ib = (const uint32_t *)f.indices + io + 3 * lo;
-        const int n = (int)(hi - lo);
-        const bool vec = (((uintptr_t)ib) & 15) == 0;
-        const long long tag = (item << 40) | lo;
+        // float4 positions: one 128-bit gather per vertex
+        const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + item);
+        const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + item) + 3 * lo;
+        lean_range<TPL, PROBE, ILV>(f, F, C, pb, ib, (int)(hi - lo), (item << 40) | lo, n_frustum,
+                                    n_tiny, sidx[ILV == 2 ? (threadIdx.x >> 5) : 0]);
+    }
+    unsigned long long cnt[2] = {n_frustum, n_tiny};
+    flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+    flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+}
 
-        for (int s0 = 0; s0 < n; s0 += STEP) {
-            const int o = s0 + TPL * lane;
-            const int nv = max(0, min(TPL, n - o));
-            uint32_t ix[3 * TPL];
-            if (TPL == 4 && vec && nv == TPL) {
-                const uint4 *v = (const uint4 *)(ib + 3 * o);
-                const uint4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
-                ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w;
-                ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
-                ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
-            } else if (TPL == 2 && vec && nv == TPL) {
-                const uint2 *v = (const uint2 *)(ib + 3 * o);
-                const uint2 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
-                ix[0] = a.x; ix[1] = a.y; ix[2] = b.x; ix[3] = b.y; ix[4] = d.x; ix[5] = d.y;
+// Meshlet lean kernel (flat table, meshes with meshlets).  Per batch of
+// triangles a warp
+//   1. gathers and projects each listed vertex once (lanes j, j+32, ...) and
+//      stores the vertex's conservative sample-space interval
+//        lo' = p' - eps_v - 0.5,  hi' = p' + eps_v - 0.5   (x and y)
+//      with eps_v the filter bound of THAT vertex (filter.cuh: the bound is
+//      per vertex — |p'| and d' of the vertex itself); a vertex not beyond
+//      the near margin stores (-inf, +inf), which blocks every decision;
+//   2. decides its triangles from 3 local indices each: over the three
+//      intervals, min lo' / max hi' give the bbox tests of lean_decide
+//      (interior, frustum, tiny), max lo' > min hi' proves a nonzero
+//      extent (not CULL_OFFSCREEN).
+// A regular batch is one meshlet (126 triangles, <= 256 unique vertices, u8
+// local indices, 4 triangles per lane).  A meshlet with more vertices runs
+// as two RAW batches of 63 triangles whose vertex list is the index stream
+// itself (189 entries, local index 3t + e).  Undecided triangles re-gather
+// their 3 object positions (L1-hot) into the fp64 queue.
+constexpr int MESH_WARPS = 8;
+
+template <bool RAW>
+__device__ __forceinline__ void mesh_batch(const curast_frame_t &f, const LeanConsts &F,
+                                           const LeanCtx &C, float4 *wI,
+                                           const float4 *__restrict__ pb,
+                                           const uint32_t *__restrict__ vsrc, int nu,
+                                           const uint32_t *__restrict__ ltri, int rb,
+                                           int rlo, int rhi, long long tagb,
+                                           unsigned &n_frustum, unsigned &n_tiny) {
+    // triangles of this batch: chunk-relative [rb, rb + 32*TPL) ∩ [rlo, rhi)
+    constexpr int TPL = RAW ? 2 : 4;
+    const int lane = C.lane;
+    // 1. listed vertices: id loads, then gathers, then math (two dependent
+    //    memory round trips per 128 vertices)
+    for (int g = 0; g < nu; g += 128) {
+        uint32_t vid[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int j = g + lane + 32 * r;
+            vid[r] = j < nu ? __ldg(vsrc + j) : 0u;
+        }
+        float4 q[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) q[r] = __ldg(pb + vid[r]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int j = g + lane + 32 * r;
+            const float D = __fmaf_rn(F.dz, q[r].z, __fmaf_rn(F.dy, q[r].y, __fmaf_rn(F.dx, q[r].x, F.d3)));
+            float2 t = __ffma2_rn(F.cx, make_float2(q[r].x, q[r].x), F.c3);
+            t = __ffma2_rn(F.cy, make_float2(q[r].y, q[r].y), t);
+            t = __ffma2_rn(F.cz, make_float2(q[r].z, q[r].z), t);
+            const float rr = rcp_approx(D);
+            const float2 P = __fmul2_rn(t, make_float2(rr, rr));
+            const float M = fmaxf(fabsf(P.x), fabsf(P.y));
+            float eps = __fmaf_rn(M, F.ed, F.exy) * rr;
+            eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, C.slack));
+            const float2 lo = __fadd2_rn(P, make_float2(-0.5f - eps, -0.5f - eps));
+            const float2 hi = __fadd2_rn(P, make_float2(eps - 0.5f, eps - 0.5f));
+            const bool ok = D > F.near_hi;
+            const float inf = __int_as_float(0x7f800000);
+            if (j < nu)
+                wI[j] = ok ? make_float4(lo.x, lo.y, hi.x, hi.y) : make_float4(-inf, -inf, inf, inf);
+        }
+    }
+    __syncwarp();
+    // 2. triangles rb + TPL*lane + k
+    uint32_t w[3] = {0u, 0u, 0u};
+    if (!RAW) {
+        const uint32_t *tw = ltri + 3 * lane;
+        w[0] = __ldg(tw);
+        w[1] = __ldg(tw + 1);
+        w[2] = __ldg(tw + 2);
+    }
+    auto loc = [&](int k, int e) -> int {
+        if (RAW) return 3 * (TPL * lane + k) + e;
+        const int b = 3 * k + e;
+        return (int)__byte_perm(w[b >> 2], 0u, 0x4440u | (unsigned)(b & 3));
+    };
+    const float Wl = C.W - 0.5f, Hl = C.H - 0.5f;
+    const int tb = rb + TPL * lane;
+    unsigned need = 0, fr = 0, valid = 0;
+#pragma unroll
+    for (int k = 0; k < TPL; ++k) {
+        const float4 A = wI[loc(k, 0)], B = wI[loc(k, 1)], Q = wI[loc(k, 2)];
+        const float mlx = fminf(A.x, fminf(B.x, Q.x)), mly = fminf(A.y, fminf(B.y, Q.y));
+        const float Mhx = fmaxf(A.z, fmaxf(B.z, Q.z)), Mhy = fmaxf(A.w, fmaxf(B.w, Q.w));
+        const float Mlx = fmaxf(A.x, fmaxf(B.x, Q.x)), Mly = fmaxf(A.y, fmaxf(B.y, Q.y));
+        const float mhx = fminf(A.z, fminf(B.z, Q.z)), mhy = fminf(A.w, fminf(B.w, Q.w));
+        // bbox provably inside (0, W) x (0, H): no frustum cull, no clamping
+        const bool interior = mlx > -0.5f && mly > -0.5f && Mhx < Wl && Mhy < Hl;
+        // nonzero extent on both axes: ceil(max) > floor(min), not offscreen
+        const bool ext = Mlx > mhx && Mly > mhy;
+        // tiny: the smallest sample >= min is > max on an axis
+        const bool tiny = C.tiny && (ceilf(mlx) > Mhx || ceilf(mly) > Mhy);
+        const bool is_tiny = interior && ext && tiny;
+        // provably outside one side: frustum cull (near margin checked: a
+        // near vertex stores infinite bounds)
+        const bool is_fr = Mhx < -0.5f || Mhy < -0.5f || mlx > Wl || mly > Hl;
+        const unsigned ok = (tb + k >= rlo && tb + k < rhi) ? 1u : 0u;
+        valid |= ok << k;
+        need |= ((is_tiny || is_fr) ? 0u : ok) << k;
+        fr |= (is_fr ? ok : 0u) << k;
+    }
+    n_frustum += __popc(fr);
+    n_tiny += __popc(valid) - __popc(need) - __popc(fr);
+    unsigned b[TPL];
+    int tot = 0;
+#pragma unroll
+    for (int k = 0; k < TPL; ++k) {
+        b[k] = __ballot_sync(0xffffffffu, (need >> k) & 1u);
+        tot += __popc(b[k]);
+    }
+    if (tot) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(C.qcount, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+        for (int k = 0; k < TPL; ++k) {
+            if ((need >> k) & 1u) {
+                float x[3], y[3], z[3];
+#pragma unroll
+                for (int e = 0; e < 3; ++e) {
+                    const float4 q = __ldg(pb + __ldg(vsrc + loc(k, e)));
+                    x[e] = q.x;
+                    y[e] = q.y;
+                    z[e] = q.z;
+                }
+                qx_write(f, (long long)base + __popc(b[k] & C.lt_mask), x, y, z, tagb + tb + k);
+            }
+            base += __popc(b[k]);
+        }
+    }
+    __syncwarp();
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(32 * MESH_WARPS, MINB) k_s1_mesh(const curast_frame_t f,
+                                                                    int64_t cbeg, int64_t cend,
+                                                                    int claim_slot) {
+    constexpr int MT = CURAST_MESHLET_TRIS, MV = CURAST_MESHLET_MAX_VERTS;
+    constexpr int MB = CURAST_MESHLET_BYTES;
+    static_assert(MV >= 3 * ((MT + 1) / 2), "RAW half-meshlet batches need their vertex slots");
+    static_assert(MB >= 12 * 32, "4 triangles x 3 bytes per lane");
+    __shared__ float4 sI[MESH_WARPS][MV];
+    float4 *wI = sI[threadIdx.x >> 5];
+    const LeanCtx C = lean_ctx(f);
+    unsigned n_frustum = 0, n_tiny = 0;
+    const int64_t total = min(cend, __ldg(f.unit_chunk_prefix + f.n_units));
+    for (;;) {
+        long long item = 0, lo = 0, hi = 0;
+        if (!lean_claim(f, C.lane, cbeg, total, claim_slot, item, lo, hi)) break;
+        LeanConsts F;
+        lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);
+        const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + item);
+        // chunk-relative 32-bit indexing from the first meshlet it touches
+        const long long m0 = lo / MT, base = m0 * MT;
+        const int rlo = (int)(lo - base), rhi = (int)(hi - base);
+        const int64_t gm0 = __ldg(f.item_ml_off + item) + m0;
+        const int64_t *voff = f.ml_voff + gm0;
+        const uint32_t *trib = (const uint32_t *)(f.ml_tris + gm0 * MB);
+        const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + item) + 3 * base;
+        const long long tagb = (item << 40) | base;
+        const int nml = (rhi + MT - 1) / MT;
+        for (int m = 0; m < nml; ++m) {
+            const int64_t vb = __ldg(voff + m);
+            const int nu = (int)(__ldg(voff + m + 1) - vb);
+            if (nu <= MV) {
+                mesh_batch<false>(f, F, C, wI, pb, f.ml_verts + vb, nu, trib + m * (MB / 4),
+                                  m * MT, rlo, min(rhi, m * MT + MT), tagb, n_frustum, n_tiny);
             } else {
-#pragma unroll
-                for (int k = 0; k < 3 * TPL; ++k) ix[k] = (k < 3 * nv) ? __ldg(ib + 3 * o + k) : 0u;
-            }
-            float px[3 * TPL], py[3 * TPL], pz[3 * TPL];
-#pragma unroll
-            for (int k = 0; k < 3 * TPL; ++k) {
-                const float4 q = __ldg(pb + ix[k]);
-                px[k] = q.x;
-                py[k] = q.y;
-                pz[k] = q.z;
-            }
-            unsigned need = 0, fr = 0;
-#pragma unroll
-            for (int t = 0; t < TPL; ++t) {
-                const unsigned bits = lean_bits(F, px + 3 * t, py + 3 * t, pz + 3 * t, W, H, slack, tiny);
-                if (t < nv) {
-                    need |= (bits & 1u) << t;
-                    fr |= (bits >> 1) << t;
-                }
-            }
-            n_frustum += __popc(fr);
-            n_tiny += nv - __popc(need) - __popc(fr);
-            unsigned b[TPL];
-            int tot = 0;
-#pragma unroll
-            for (int t = 0; t < TPL; ++t) {
-                b[t] = __ballot_sync(0xffffffffu, (need >> t) & 1u);
-                tot += __popc(b[t]);
-            }
-            if (tot) {
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(qcount, (unsigned long long)tot);
-                base = __shfl_sync(0xffffffffu, base, 0);
-#pragma unroll
-                for (int t = 0; t < TPL; ++t) {
-                    if ((need >> t) & 1u) {
-                        const long long slot = (long long)base + __popc(b[t] & lt_mask);
-                        if (slot < f.qx_cap) {
-                            // positions travel with the entry: the fp64 kernel
-                            // does not re-gather them from HBM
-                            int64_t *e = f.qx + CURAST_QX_WORDS * slot;
-                            *(float4 *)e = make_float4(px[3 * t], py[3 * t], pz[3 * t], px[3 * t + 1]);
-                            *(float4 *)(e + 2) = make_float4(py[3 * t + 1], pz[3 * t + 1],
-                                                             px[3 * t + 2], py[3 * t + 2]);
-                            *(float2 *)(e + 4) = make_float2(pz[3 * t + 2], 0.0f);
-                            e[CURAST_QX_TAG] = tag + o + t;
-                        }
-                    }
-                    base += __popc(b[t]);
-                }
+                constexpr int H1 = (MT + 1) / 2;
+                mesh_batch<true>(f, F, C, wI, pb, ib + 3 * m * MT, 3 * H1, nullptr, m * MT,
+                                 rlo, min(rhi, m * MT + H1), tagb, n_frustum, n_tiny);
+                mesh_batch<true>(f, F, C, wI, pb, ib + 3 * (m * MT + H1), 3 * (MT - H1), nullptr,
+                                 m * MT + H1, max(rlo, m * MT + H1), min(rhi, m * MT + MT), tagb,
+                                 n_frustum, n_tiny);
             }
         }
     }

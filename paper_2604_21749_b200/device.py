@@ -21,6 +21,7 @@ Layout in HBM (per GPU):
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -104,6 +105,13 @@ class DeviceMesh:
             return g[:3] + (q + 0.5) / 65536.0 * g[3:]
         raise ValueError("unsupported position conversion")
 
+    def meshlets(self):
+        """(ml_voff int64[nm+1], ml_verts int32[], ml_tris uint8[nm*3*MT]) of
+        this mesh's u32 index stream, built once on the device (cached)."""
+        if getattr(self, "_meshlets", None) is None:
+            self._meshlets = build_meshlets(self.indices_u32(), self.triangle_count)
+        return self._meshlets
+
     def indices_u32(self):
         if self.idx_format == N.IDX_U32:
             return self.indices
@@ -117,6 +125,46 @@ class DeviceMesh:
         win = lo | (hi << 32)
         rel = (win >> (bit & 31)) & ((1 << b) - 1) if b < 63 else win
         return (rel + mn).to(torch.int64).to(torch.int32)
+
+
+def build_meshlets(indices: torch.Tensor, triangle_count: int, block: int = 1 << 16):
+    """Meshlets of a u32 index stream (curast.h CURAST_MESHLET_TRIS).
+
+    Meshlet m holds triangles [m*MT, (m+1)*MT) in stream order (global
+    triangle IDs stay implicit); its unique vertex ids ascending, and every
+    triangle as 3 u8 positions in that list.  A meshlet with more than
+    CURAST_MESHLET_MAX_VERTS unique vertices keeps a count above the limit and
+    no valid u8 data (the kernel reads the index stream for it)."""
+    MT, MB = N.MESHLET_TRIS, N.MESHLET_BYTES
+    dev = indices.device
+    T = int(triangle_count)
+    nm = -(-T // MT)
+    if nm == 0:
+        return (torch.zeros(1, dtype=torch.int64, device=dev),
+                torch.zeros(0, dtype=torch.int32, device=dev),
+                torch.zeros(0, dtype=torch.uint8, device=dev))
+    ix = indices[:3 * T].to(torch.int64) & 0xFFFFFFFF
+    pad = nm * 3 * MT - 3 * T
+    if pad:
+        ix = torch.cat([ix, ix[-1:].expand(pad)])
+    rows = ix.view(nm, 3 * MT)
+    counts, verts, tris = [], [], []
+    for b0 in range(0, nm, block):
+        r = rows[b0:b0 + block]
+        srt, _ = torch.sort(r, dim=1)
+        new = torch.ones_like(srt, dtype=torch.bool)
+        new[:, 1:] = srt[:, 1:] != srt[:, :-1]
+        rank = torch.cumsum(new, dim=1) - 1
+        loc = torch.gather(rank, 1, torch.searchsorted(srt, r))
+        counts.append(new.sum(dim=1))
+        verts.append(srt[new].to(torch.int32))
+        t8 = torch.zeros((r.shape[0], MB), dtype=torch.uint8, device=dev)
+        t8[:, :3 * MT] = loc.clamp_(max=255).to(torch.uint8)
+        tris.append(t8.reshape(-1))
+    nu = torch.cat(counts)
+    voff = torch.zeros(nm + 1, dtype=torch.int64, device=dev)
+    voff[1:] = torch.cumsum(nu, 0)
+    return voff, torch.cat(verts), torch.cat(tris)
 
 
 _CACHE_ATTR = "_curast_device_copies"
@@ -188,6 +236,26 @@ class SceneGeometry:
         else:
             self.positions = torch.cat(pos_parts)
             self.indices = torch.cat(idx_parts)
+        # meshlets feed the f32 / u32 meshlet stage-1 kernel (CURAST_MESHLETS=1;
+        # the per-triangle kernel is the measured default)
+        self.ml_off = [0] * len(dms)
+        self.ml_voff = self.ml_verts = self.ml_tris = None
+        if (self.pos_format == N.POS_F32 and self.idx_format == N.IDX_U32
+                and os.environ.get("CURAST_MESHLETS", "0") == "1"):
+            vo_parts, vt_parts, tr_parts = [], [], []
+            nm = nvl = 0
+            for k, d in enumerate(dms):
+                voff, verts, tris = d.meshlets()
+                self.ml_off[k] = nm
+                vo_parts.append(voff[:-1] + nvl)
+                vt_parts.append(verts)
+                tr_parts.append(tris)
+                nm += voff.numel() - 1
+                nvl += verts.numel()
+            vo_parts.append(torch.full((1,), nvl, dtype=torch.int64, device=device))
+            self.ml_voff = torch.cat(vo_parts)
+            self.ml_verts = vt_parts[0] if len(vt_parts) == 1 else torch.cat(vt_parts)
+            self.ml_tris = tr_parts[0] if len(tr_parts) == 1 else torch.cat(tr_parts)
         self.keepalive = dms
 
 

@@ -161,6 +161,7 @@ class PreparedFrame:
         n = self.n_items
         vtx_off = np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64)
         idx_off = np.asarray([geo.idx_off[i] for i in ctx.item_mesh], dtype=np.int64)
+        ml_off = np.asarray([geo.ml_off[i] for i in ctx.item_mesh], dtype=np.int64)
         p = projection_vector(camera)
         p0, p1 = float(p[0]), float(p[1])
         self.p0, self.p1 = p0, p1
@@ -211,6 +212,7 @@ class PreparedFrame:
         k_mw = up.add(ctx.item_mw.reshape(-1))
         k_vo = up.add(vtx_off)
         k_io = up.add(idx_off)
+        k_mo = up.add(ml_off)
         k_f = up.add(filt.reshape(-1))
         k_q = up.add(qgrid.reshape(-1).astype(np.float64))
         k_pk = up.add(pack.reshape(-1))
@@ -244,6 +246,11 @@ class PreparedFrame:
         f.item_filter = up.ptr(k_f)
         f.item_qgrid = up.ptr(k_q)
         f.item_pack = up.ptr(k_pk)
+        if geo.ml_voff is not None:
+            f.item_ml_off = up.ptr(k_mo)
+            f.ml_voff = geo.ml_voff.data_ptr()
+            f.ml_verts = geo.ml_verts.data_ptr()
+            f.ml_tris = geo.ml_tris.data_ptr()
         f.instanced = int(self.instanced)
         f.use_filter = int(self.use_filter)
         f.n_groups = len(ctx.group_item_count)
@@ -381,7 +388,8 @@ class PreparedFrame:
                                 tiles=int(s2[4]), fragments=int(s2[3]))
         st.stage3 = Stage3Stats(entries=int(c[N.C_Q3]), fragments=int(c[N.C_S3]))
         st.merge_s, st.stage1_s, st.stage2_s, st.stage3_s = secs
-        st.exact_fallbacks = int(c[N.C_QX]) + int(c[N.C_EXACT])
+        st.proved_fp32 = int(c[N.C_PROVED])
+        st.exact_fallbacks = int(c[N.C_QX]) + int(c[N.C_EXACT]) - st.proved_fp32
         return st
 
 

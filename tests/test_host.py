@@ -239,3 +239,35 @@ def test_device_copy_cache_is_identity_checked():
         gc.collect()
     dv.drop_device_copies([m])
     assert dv.device_mesh(m, cpu) is not b
+
+
+def test_build_meshlets_roundtrip_and_overflow():
+    """device.build_meshlets: every triangle's u8 local indices map back to its
+    vertex ids; meshlets with > CURAST_MESHLET_MAX_VERTS vertices are marked
+    by their count (the kernel then reads the index stream)."""
+    import torch
+
+    from paper_2604_21749_b200 import device as dv
+    for T, scatter in ((1000, False), (777, True)):
+        rng = np.random.default_rng(T)
+        if scatter:
+            idx = rng.integers(0, 5000, size=3 * T).astype(np.uint32)
+        else:
+            idx = grid_indices(30)[:3 * T].astype(np.uint32)
+        voff, verts, tris = dv.build_meshlets(torch.from_numpy(idx.view(np.int32)), T)
+        voff, verts, tris = voff.numpy(), verts.numpy(), tris.numpy()
+        MT, MB = N.MESHLET_TRIS, N.MESHLET_BYTES
+        nm = -(-T // MT)
+        assert len(voff) == nm + 1 and len(tris) == nm * MB
+        for m in range(nm):
+            vl = verts[voff[m]:voff[m + 1]]
+            assert np.all(np.diff(vl.astype(np.int64)) > 0)      # ascending, unique
+            tt = np.arange(m * MT, min(T, m * MT + MT))
+            want = idx.reshape(-1, 3)[tt]
+            if len(vl) > N.MESHLET_MAX_VERTS:
+                assert scatter
+                continue
+            loc = tris[m * MB:m * MB + 3 * len(tt)].reshape(-1, 3)
+            assert np.array_equal(vl[loc].astype(np.uint32), want)
+        if scatter:
+            assert (np.diff(voff) > N.MESHLET_MAX_VERTS).any()
