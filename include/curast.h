@@ -88,10 +88,13 @@ enum curast_error {
 
 /* meshlets: triangles per meshlet (a strip of 63 quads has 128 vertices),
  * bytes per meshlet triangle record (3 u8 per triangle, padded), largest
- * vertex list with u8 indices */
+ * vertex list with u8 slot indices: vertex j of the list is stored in the
+ * kernel's shared-memory slot j + j/16 (one pad slot per 16 keeps the
+ * lookups of strip meshes bank-conflict free), and the u8 triangle record
+ * holds that slot number */
 #define CURAST_MESHLET_TRIS 126
 #define CURAST_MESHLET_BYTES 384
-#define CURAST_MESHLET_MAX_VERTS 256
+#define CURAST_MESHLET_MAX_VERTS 240
 
 /* fp64 work-queue entry: 6 int64 words (48 B) */
 #define CURAST_QX_WORDS 6
@@ -115,13 +118,21 @@ typedef struct curast_frame {
     /* ---- meshlets of u32 index streams (optional: NULL = none) ----
      * triangle t of a mesh lies in meshlet t / CURAST_MESHLET_TRIS; a meshlet
      * lists its unique vertices (ascending mesh-local ids) and stores each
-     * triangle as 3 u8 indices into that list.  A meshlet with more than
+     * triangle as 3 u8 slot numbers (vertex j -> slot j + j/16).  A meshlet with more than
      * CURAST_MESHLET_MAX_VERTS vertices has no u8 form: its triangles are
      * read from the index stream instead.                                  */
     const int64_t *item_ml_off;       /* first meshlet of the item's mesh     */
     const int64_t *ml_voff;           /* int64[n_meshlets+1] into ml_verts    */
     const uint32_t *ml_verts;         /* mesh-local vertex ids                */
     const uint8_t *ml_tris;           /* uint8[n_meshlets][CURAST_MESHLET_BYTES] */
+    /* ---- per-chunk object-space boxes (POS_F32 + IDX_U32; optional) ----
+     * box b of a mesh bounds the vertices of its triangles
+     * [b*C, (b+1)*C), C = curast_chunk_tris(0): float[8] = min xyz, 0,
+     * max xyz, 0.  Stage 1 projects a chunk's box corners once and takes
+     * the per-triangle fast path when the whole chunk is provably in front
+     * of the near margin and inside the viewport.                          */
+    const int64_t *item_cb_off;       /* first box of the item's mesh         */
+    const float *chunk_box;           /* float[n_boxes][8]                    */
     /* ---- instancing groups (pipeline.py:114-135) ---- */
     int32_t instanced;                /* 1: stage1_instanced_range semantics  */
     int32_t use_filter;               /* 1: fp32 cull filter + fp64 fallback  */

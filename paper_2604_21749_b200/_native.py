@@ -26,7 +26,8 @@ INST_BLOCK = 16          # CURAST_INST_BLOCK: instances per instanced work unit
 QX_WORDS = 6
 MESHLET_TRIS = 126       # CURAST_MESHLET_TRIS
 MESHLET_BYTES = 384      # CURAST_MESHLET_BYTES
-MESHLET_MAX_VERTS = 256  # CURAST_MESHLET_MAX_VERTS
+MESHLET_MAX_VERTS = 240  # CURAST_MESHLET_MAX_VERTS (u8 slot j + j//16)
+S1_CHUNK = 16 * MESHLET_TRIS   # curast_chunk_tris(0): flat stage-1 chunk
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -44,6 +45,7 @@ class CurastFrame(ctypes.Structure):
         ("item_vtx_off", _P), ("item_idx_off", _P), ("item_filter", _P),
         ("item_qgrid", _P), ("item_pack", _P),
         ("item_ml_off", _P), ("ml_voff", _P), ("ml_verts", _P), ("ml_tris", _P),
+        ("item_cb_off", _P), ("chunk_box", _P),
         ("instanced", _I32), ("use_filter", _I32),
         ("n_groups", _I64), ("group_prefix", _P), ("group_item_off", _P),
         ("group_item_count", _P), ("group_items", _P),

@@ -112,6 +112,13 @@ class DeviceMesh:
             self._meshlets = build_meshlets(self.indices_u32(), self.triangle_count)
         return self._meshlets
 
+    def chunk_boxes(self):
+        """Per-chunk object-space boxes (POS_F32 meshes), built once."""
+        if getattr(self, "_chunk_boxes", None) is None:
+            self._chunk_boxes = build_chunk_boxes(self.positions, self.indices_u32(),
+                                                  self.triangle_count)
+        return self._chunk_boxes
+
     def indices_u32(self):
         if self.idx_format == N.IDX_U32:
             return self.indices
@@ -132,7 +139,7 @@ def build_meshlets(indices: torch.Tensor, triangle_count: int, block: int = 1 <<
 
     Meshlet m holds triangles [m*MT, (m+1)*MT) in stream order (global
     triangle IDs stay implicit); its unique vertex ids ascending, and every
-    triangle as 3 u8 positions in that list.  A meshlet with more than
+    triangle as 3 u8 slot numbers (entry j -> slot j + j//16).  A meshlet with more than
     CURAST_MESHLET_MAX_VERTS unique vertices keeps a count above the limit and
     no valid u8 data (the kernel reads the index stream for it)."""
     MT, MB = N.MESHLET_TRIS, N.MESHLET_BYTES
@@ -159,12 +166,36 @@ def build_meshlets(indices: torch.Tensor, triangle_count: int, block: int = 1 <<
         counts.append(new.sum(dim=1))
         verts.append(srt[new].to(torch.int32))
         t8 = torch.zeros((r.shape[0], MB), dtype=torch.uint8, device=dev)
-        t8[:, :3 * MT] = loc.clamp_(max=255).to(torch.uint8)
+        # u8 shared-memory slot of list entry j: j + j // 16 (curast.h)
+        t8[:, :3 * MT] = (loc + loc // 16).clamp_(max=255).to(torch.uint8)
         tris.append(t8.reshape(-1))
     nu = torch.cat(counts)
     voff = torch.zeros(nm + 1, dtype=torch.int64, device=dev)
     voff[1:] = torch.cumsum(nu, 0)
     return voff, torch.cat(verts), torch.cat(tris)
+
+
+def build_chunk_boxes(pos4: torch.Tensor, indices: torch.Tensor, triangle_count: int,
+                      block: int = 1 << 12):
+    """float32[nb, 8] object-space boxes (min xyz, 0, max xyz, 0) of the
+    vertices of triangles [b*C, (b+1)*C), C = the flat stage-1 chunk."""
+    C = N.S1_CHUNK
+    dev = pos4.device
+    T = int(triangle_count)
+    nb = -(-T // C)
+    out = torch.zeros((nb, 8), dtype=torch.float32, device=dev)
+    if nb == 0:
+        return out
+    ix = indices[:3 * T].to(torch.int64) & 0xFFFFFFFF
+    pad = nb * 3 * C - 3 * T
+    if pad:
+        ix = torch.cat([ix, ix[-1:].expand(pad)])
+    rows = ix.view(nb, 3 * C)
+    for b0 in range(0, nb, block):
+        p = pos4[rows[b0:b0 + block], :3]                      # (b, 3C, 3)
+        out[b0:b0 + block, 0:3] = p.amin(dim=1)
+        out[b0:b0 + block, 4:7] = p.amax(dim=1)
+    return out
 
 
 _CACHE_ATTR = "_curast_device_copies"
@@ -236,6 +267,17 @@ class SceneGeometry:
         else:
             self.positions = torch.cat(pos_parts)
             self.indices = torch.cat(idx_parts)
+        # chunk boxes feed the f32 / u32 stage-1 fast path
+        self.cb_off = [0] * len(dms)
+        self.chunk_box = None
+        if self.pos_format == N.POS_F32 and self.idx_format == N.IDX_U32:
+            parts, nb = [], 0
+            for k, d in enumerate(dms):
+                b = d.chunk_boxes()
+                self.cb_off[k] = nb
+                parts.append(b)
+                nb += b.shape[0]
+            self.chunk_box = parts[0] if len(parts) == 1 else torch.cat(parts)
         # meshlets feed the f32 / u32 meshlet stage-1 kernel (CURAST_MESHLETS=1;
         # the per-triangle kernel is the measured default)
         self.ml_off = [0] * len(dms)

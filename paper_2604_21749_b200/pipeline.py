@@ -162,6 +162,7 @@ class PreparedFrame:
         vtx_off = np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64)
         idx_off = np.asarray([geo.idx_off[i] for i in ctx.item_mesh], dtype=np.int64)
         ml_off = np.asarray([geo.ml_off[i] for i in ctx.item_mesh], dtype=np.int64)
+        cb_off = np.asarray([geo.cb_off[i] for i in ctx.item_mesh], dtype=np.int64)
         p = projection_vector(camera)
         p0, p1 = float(p[0]), float(p[1])
         self.p0, self.p1 = p0, p1
@@ -213,6 +214,7 @@ class PreparedFrame:
         k_vo = up.add(vtx_off)
         k_io = up.add(idx_off)
         k_mo = up.add(ml_off)
+        k_co = up.add(cb_off)
         k_f = up.add(filt.reshape(-1))
         k_q = up.add(qgrid.reshape(-1).astype(np.float64))
         k_pk = up.add(pack.reshape(-1))
@@ -246,6 +248,9 @@ class PreparedFrame:
         f.item_filter = up.ptr(k_f)
         f.item_qgrid = up.ptr(k_q)
         f.item_pack = up.ptr(k_pk)
+        if geo.chunk_box is not None:
+            f.item_cb_off = up.ptr(k_co)
+            f.chunk_box = geo.chunk_box.data_ptr()
         if geo.ml_voff is not None:
             f.item_ml_off = up.ptr(k_mo)
             f.ml_voff = geo.ml_voff.data_ptr()

@@ -267,7 +267,9 @@ def test_build_meshlets_roundtrip_and_overflow():
             if len(vl) > N.MESHLET_MAX_VERTS:
                 assert scatter
                 continue
-            loc = tris[m * MB:m * MB + 3 * len(tt)].reshape(-1, 3)
+            slot = tris[m * MB:m * MB + 3 * len(tt)].reshape(-1, 3).astype(np.int64)
+            loc = slot - slot // 17                              # inverse of j + j // 16
+            assert np.array_equal(loc + loc // 16, slot)
             assert np.array_equal(vl[loc].astype(np.uint32), want)
         if scatter:
             assert (np.diff(voff) > N.MESHLET_MAX_VERTS).any()
