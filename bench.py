@@ -236,7 +236,8 @@ def run_ours(args):
             "gpu_launches": launches_per_step * K,
         }
         if not args.profile:
-            result["e2e"] = e2e_measure(dl, cam, cfg, total, world)
+            result["e2e"] = e2e_measure(dl, cam, cfg, total, world, steps=min(args.steps, 10),
+                                        warmup=max(3, args.warmup))
             if world == 1 and not args.no_cpu_baseline:
                 result["cpu_baseline"] = cpu_baseline(scene, cam, dl, total)
     if world > 1:
@@ -245,7 +246,7 @@ def run_ours(args):
     return result
 
 
-def e2e_measure(dl, cam, cfg, total, world):
+def e2e_measure(dl, cam, cfg, total, world, steps=5, warmup=3):
     """Through the public drop-in call: render_draw_list(dl, cam, cfg) then
     Framebuffer.words (the reference's host np.uint64 array).  Per step: host
     descriptor build + pinned H2D, stages 1-3, counters + VB D2H.  Geometry
@@ -256,9 +257,10 @@ def e2e_measure(dl, cam, cfg, total, world):
     import paper_2604_21749_b200 as cr
     from paper_2604_21749_b200 import device as dv
     from paper_2604_21749_b200.pipeline import PreparedFrame
-    fb, st = cr.render_draw_list(dl, cam, cfg)
-    _ = fb.words
-    reps = 5
+    for _ in range(max(1, warmup)):
+        fb, st = cr.render_draw_list(dl, cam, cfg)
+        words = fb.words
+    reps = max(1, steps)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(reps):
