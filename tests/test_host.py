@@ -273,3 +273,51 @@ def test_build_meshlets_roundtrip_and_overflow():
             assert np.array_equal(vl[loc].astype(np.uint32), want)
         if scatter:
             assert (np.diff(voff) > N.MESHLET_MAX_VERTS).any()
+
+
+def _grazing_transforms(rng, cam, n):
+    """Instance transforms whose boxes touch or nearly touch frustum planes:
+    random rotations / scales, translated so the box's extreme corner lands
+    on a plane (plus tiny offsets of a few ulps either way)."""
+    from paper_2604_21749_b200.scene import frustum_planes, transformed_aabb
+    planes = frustum_planes(cam)
+    aabb = np.array([[-0.5, -0.5, -0.5], [0.5, 0.5, 0.5]])
+    out = []
+    for k in range(n):
+        q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        T = np.eye(4)
+        T[:3, :3] = q * rng.uniform(0.1, 2.0)
+        T[:3, 3] = rng.uniform(-8, 8, size=3) + np.array([0, 0, -10.0])
+        if k % 2 == 0:
+            pl = planes[rng.integers(0, len(planes))]
+            box = transformed_aabb(aabb, T)
+            c = np.where(pl[:3] < 0.0, box[1], box[0])
+            v = float(pl[:3] @ c + pl[3])
+            n3 = pl[:3] / np.dot(pl[:3], pl[:3])
+            T[:3, 3] -= v * n3                        # corner onto the plane
+            T[:3, 3] += n3 * rng.choice([0.0, 1e-15, -1e-15, 1e-12, -1e-12])
+        out.append(T)
+    return out
+
+
+def test_batched_cull_matches_per_instance_path():
+    """build_draw_list's batched, certified cull (scene._node_visibility)
+    gives the reference's items, order and prefix sums (scenecore.py:240-265,
+    restated per instance in oracle/host.py), including boxes that graze the
+    frustum planes."""
+    from paper_2604_21749_b200.scene import Mesh, SceneNode
+    rng = np.random.default_rng(11)
+    cam = Camera.look_at((0.0, 0.0, 2.0), (0.0, 0.0, -10.0), width=640, height=480)
+    mesh = Mesh(positions=np.zeros((3, 3)), indices=np.array([0, 1, 2], dtype=np.uint32),
+                triangle_count=1, aabb=np.array([[-0.5, -0.5, -0.5], [0.5, 0.5, 0.5]]))
+    scene = [SceneNode(mesh=mesh, transforms=_grazing_transforms(rng, cam, 400)),
+             SceneNode(mesh=mesh, transforms=_grazing_transforms(rng, cam, 5)),
+             SceneNode(mesh=mesh, transforms=_grazing_transforms(rng, cam, 1000))]
+    dl = build_draw_list(scene, cam)
+    ref = oh.build_draw_list(scene, cam)
+    assert len(dl.items) == len(ref.items)
+    for a, b in zip(dl.items, ref.items):
+        assert a.node_index == b.node_index
+        assert np.array_equal(np.asarray(a.instance_transform), b.transform)
+    assert np.array_equal(dl.prefix_sums, ref.prefix)
+    assert 0 < len(dl.items) < 1405
