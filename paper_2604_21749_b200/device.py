@@ -61,6 +61,17 @@ class DeviceMesh:
             self.pos_bound = gmin + np.abs(self.qgrid[3:])
             self.vertex_count = len(coords)
             self._host_f64 = None
+        elif isinstance(pos, np.ndarray) and pos.dtype == np.float32:
+            # stored f32 (e.g. a TRIMESH1 payload): exact by construction
+            p32 = pos.reshape(-1, 3)
+            self.vertex_count = len(p32)
+            self.qgrid = np.zeros(6)
+            self.pos_bound = (np.abs(p32).max(axis=0).astype(np.float64) if len(p32)
+                              else np.zeros(3))
+            self.pos_format = N.POS_F32
+            p4 = np.zeros((len(p32), 4), dtype=np.float32)
+            p4[:, :3] = p32
+            self.positions = torch.from_numpy(p4).to(device)
         else:
             p64 = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
             p32 = p64.astype(np.float32)

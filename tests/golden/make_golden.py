@@ -266,3 +266,41 @@ def main_resolve():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "resolve":
     main_resolve()
+
+
+def main_trimesh():
+    """TRIMESH1 fixtures written by the reference's save_mesh (raw, quantized +
+    packed, with uvs and colours) plus what its load_mesh_asset returns."""
+    trirast, conftest = _import_reference()
+    from trirast.geomcodec import compress_indices, load_mesh_asset, quantize_positions, save_mesh
+    from trirast.scenecore import Mesh as RMesh
+    from trirast.scenedesc import make_sphere, make_tessellated_quad
+    out = {}
+    sph = make_sphere(12, 16, radius=0.8)
+    quad = make_tessellated_quad(6)
+    q_pos = quantize_positions(sph.positions_f64(), sph.aabb)
+    p_idx = compress_indices(sph.indices_u32())
+    cases = {
+        "raw": sph,
+        "compressed": RMesh(positions=q_pos, indices=p_idx, triangle_count=sph.triangle_count,
+                            aabb=sph.aabb, vertex_colors=sph.vertex_colors, name="c"),
+        "uvquad": quad,
+    }
+    for name, mesh in cases.items():
+        path = os.path.join(HERE, f"mesh_{name}.trimesh")
+        save_mesh(path, mesh)
+        m = load_mesh_asset(path)
+        out[f"{name}_positions"] = m.positions_f64()
+        out[f"{name}_indices"] = m.indices_u32()
+        out[f"{name}_aabb"] = np.asarray(m.aabb, dtype=np.float64)
+        out[f"{name}_ntris"] = np.int64(m.triangle_count)
+        if m.uvs is not None:
+            out[f"{name}_uvs"] = np.asarray(m.uvs)
+        if m.vertex_colors is not None:
+            out[f"{name}_colors"] = np.asarray(m.vertex_colors)
+    np.savez_compressed(os.path.join(HERE, "trimesh.npz"), **out)
+    print("wrote trimesh fixtures")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trimesh":
+    main_trimesh()
