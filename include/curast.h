@@ -243,6 +243,33 @@ typedef struct curast_resolve {
 } curast_resolve_t;
 
 int curast_resolve(const curast_resolve_t *r, void *stream);
+
+/* ---- debug views (resolvepass.py:417-490 debug_view) ----
+ * mode 0 'depth' (log-scaled grey), 1 'stageID', 2 'bboxSize', 3 'meshID'.
+ * Depth mode first reduces the covered pixels' depth range into scratch. */
+typedef struct curast_debug {
+    const uint64_t *fb;
+    int64_t width, height;
+    int32_t mode;
+    int32_t pos_format, idx_format;
+    int64_t n_items;
+    const int64_t *prefix;            /* int64[n_items+1]                      */
+    const int64_t *item_vtx_off;
+    const int64_t *item_idx_off;
+    const void *positions;
+    const void *indices;
+    const double *item_qgrid;
+    const int64_t *item_pack;
+    const double *item_xform;         /* double[n_items][16] instance transform */
+    double view[16];                  /* camera view_transform, row-major      */
+    double p0, p1, near;
+    int64_t small_max, medium_max;
+    uint8_t background[4];
+    uint8_t *out_rgba;                /* uint8[height*width*4]                 */
+    uint32_t *scratch;                /* 2 words (depth mode)                  */
+} curast_debug_t;
+
+int curast_debug_view(const curast_debug_t *d, void *stream);
 int curast_downsample(const uint8_t *src, int64_t width, int64_t height,
                       int32_t factor, uint8_t *dst, void *stream);
 

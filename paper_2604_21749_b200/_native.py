@@ -62,6 +62,19 @@ class CurastFrame(ctypes.Structure):
     ]
 
 
+class CurastDebug(ctypes.Structure):
+    """Mirror of ``curast_debug_t``."""
+
+    _fields_ = [
+        ("fb", _P), ("width", _I64), ("height", _I64), ("mode", _I32),
+        ("pos_format", _I32), ("idx_format", _I32), ("n_items", _I64), ("prefix", _P),
+        ("item_vtx_off", _P), ("item_idx_off", _P), ("positions", _P), ("indices", _P),
+        ("item_qgrid", _P), ("item_pack", _P), ("item_xform", _P), ("view", _D * 16),
+        ("p0", _D), ("p1", _D), ("near", _D), ("small_max", _I64), ("medium_max", _I64),
+        ("background", ctypes.c_uint8 * 4), ("out_rgba", _P), ("scratch", _P),
+    ]
+
+
 class CurastResolve(ctypes.Structure):
     """Mirror of ``curast_resolve_t``."""
 
@@ -112,6 +125,8 @@ def lib():
     L.curast_min_u64.argtypes = [_P, _P, _I64, _P]
     L.curast_resolve.restype = _I32
     L.curast_resolve.argtypes = [ctypes.POINTER(CurastResolve), _P]
+    L.curast_debug_view.restype = _I32
+    L.curast_debug_view.argtypes = [ctypes.POINTER(CurastDebug), _P]
     L.curast_downsample.restype = _I32
     L.curast_downsample.argtypes = [_P, _I64, _I64, _I32, _P, _P]
     if L.curast_abi_version() != ABI_VERSION:
@@ -124,7 +139,7 @@ EXPORTED_SYMBOLS = (
     "curast_abi_version", "curast_last_error", "curast_chunk_tris",
     "curast_frame_clear", "curast_stage1", "curast_stage2", "curast_stage3",
     "curast_render", "curast_fill_u64", "curast_min_u64", "curast_filter_check",
-    "curast_resolve", "curast_downsample",
+    "curast_resolve", "curast_downsample", "curast_debug_view",
 )
 
 

@@ -267,6 +267,148 @@ int sms() {
     return n > 0 ? n : 148;
 }
 
+
+// ------------------------------------------------------------ debug views
+// resolvepass.py:417-490.  depth: grey = rint(255 (1 - log(d/lo)/log(hi/lo)))
+// over the covered pixels' depth range; meshID: palette of the owning item;
+// stageID / bboxSize: the winning triangle re-transformed as the reference
+// does ((obj @ T^T) @ view^T, left-to-right 4-term sums) and routed by
+// classify_route (pipeline.py, kernels.clip_near for near crossers).
+__constant__ uint8_t kStageColor[4][4] = {
+    {80, 190, 90, 255}, {235, 205, 60, 255}, {225, 70, 70, 255}, {255, 0, 255, 255}};
+
+__global__ void k_debug_range(const uint64_t *fb, int64_t npix, uint32_t *scratch) {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = fb[p];
+        if (w == ~0ull) continue;
+        const uint32_t bits = (uint32_t)(w >> 36) << 3;     // positive f32: uint order
+        lo = min(lo, bits);
+        hi = max(hi, bits);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(scratch, lo);
+        atomicMax(scratch + 1, hi);
+    }
+}
+
+// 0 STAGE1, 1 STAGE2_DIRECT, 2 STAGE3_TILED, 3 None; area out
+__device__ __forceinline__ int debug_route(const double *vx, const double *vy, const double *vz,
+                                           double p0, double p1, double near, int64_t W,
+                                           int64_t H, int64_t small_max, int64_t medium_max,
+                                           int64_t &area) {
+    area = 0;
+    const double d0 = -vz[0], d1 = -vz[1], d2 = -vz[2];
+    if (d0 < near && d1 < near && d2 < near) return 3;
+    const bool cross = d0 < near || d1 < near || d2 < near;
+    double px[4], py[4], pz[4];
+    int n = 3;
+    if (cross) {
+        n = clip_near(vx, vy, vz, near, px, py, pz);
+    } else {
+        for (int k = 0; k < 3; ++k) { px[k] = vx[k]; py[k] = vy[k]; pz[k] = vz[k]; }
+    }
+    if (n == 0) return 3;
+    double mnx = 0, mxx = 0, mny = 0, mxy = 0;
+    for (int k = 0; k < n; ++k) {
+        double d = -pz[k];
+        d = d < near ? near : d;                                   // np.maximum
+        const double sx = M(M(A(D(M(px[k], p0), d), 1.0), 0.5), (double)W);
+        const double sy = M(M(S(1.0, D(M(py[k], p1), d)), 0.5), (double)H);
+        if (k == 0) { mnx = mxx = sx; mny = mxy = sy; }
+        mnx = fmin(mnx, sx); mxx = fmax(mxx, sx);
+        mny = fmin(mny, sy); mxy = fmax(mxy, sy);
+    }
+    const int64_t ix0 = max((int64_t)floor(mnx), (int64_t)0), ix1 = min((int64_t)ceil(mxx), W);
+    const int64_t iy0 = max((int64_t)floor(mny), (int64_t)0), iy1 = min((int64_t)ceil(mxy), H);
+    if (ix0 >= ix1 || iy0 >= iy1) return 3;
+    area = (ix1 - ix0) * (iy1 - iy0);
+    if (cross || area >= medium_max) return 2;
+    if (area >= small_max) return 1;
+    return 0;
+}
+
+template <int PF, int IF>
+__global__ void k_debug_view(const curast_debug_t d) {
+    curast_frame_t f;
+    f.pos_format = d.pos_format;
+    f.idx_format = d.idx_format;
+    f.positions = d.positions;
+    f.indices = d.indices;
+    f.item_vtx_off = d.item_vtx_off;
+    f.item_idx_off = d.item_idx_off;
+    f.item_qgrid = d.item_qgrid;
+    f.item_pack = d.item_pack;
+    const int64_t npix = d.width * d.height;
+    double lo = 0.0, hi = 0.0, span = 1.0;
+    if (d.mode == 0) {
+        lo = (double)__uint_as_float(d.scratch[0]);
+        hi = (double)__uint_as_float(d.scratch[1]);
+        span = hi > lo ? log(D(hi, lo)) : 1.0;
+    }
+    for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < npix;
+         pix += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = d.fb[pix];
+        uint8_t *o = d.out_rgba + 4 * pix;
+        uint8_t c[4] = {d.background[0], d.background[1], d.background[2], d.background[3]};
+        if (w != ~0ull) {
+            if (d.mode == 0) {
+                const double dep = (double)__uint_as_float((uint32_t)(w >> 36) << 3);
+                const double shade = hi > lo ? D(log(D(dep, lo)), span) : 0.0;
+                double g = rint(M(255.0, S(1.0, shade)));
+                g = g < 0.0 ? 0.0 : (g > 255.0 ? 255.0 : g);
+                c[0] = c[1] = c[2] = (uint8_t)g;
+                c[3] = 255;
+            } else {
+                const int64_t gid = (int64_t)(w & ((1ull << 36) - 1));
+                int64_t a = 0, b = d.n_items + 1;
+                while (a < b) {
+                    const int64_t mid = (a + b) >> 1;
+                    if (d.prefix[mid] <= gid) a = mid + 1; else b = mid;
+                }
+                const int64_t item = a - 1;
+                if (d.mode == 3) {
+                    const int k = (int)(item & 255);
+                    c[0] = (uint8_t)((53 + 97 * k) & 255);
+                    c[1] = (uint8_t)((131 + 61 * k) & 255);
+                    c[2] = (uint8_t)((197 + 151 * k) & 255);
+                    c[3] = 255;
+                } else {
+                    const int64_t local = gid - d.prefix[item];
+                    const double *T = d.item_xform + 16 * item;
+                    double vx[3], vy[3], vz[3];
+                    for (int k = 0; k < 3; ++k) {
+                        const uint32_t vi = fetch_index<IF>(f, item, 3 * local + k);
+                        double x, y, z;
+                        fetch_pos64<PF>(f, item, vi, x, y, z);
+                        double wv[4];
+                        for (int r = 0; r < 4; ++r)
+                            wv[r] = A(A(A(M(x, T[4 * r]), M(y, T[4 * r + 1])), M(z, T[4 * r + 2])),
+                                      M(1.0, T[4 * r + 3]));
+                        double vv[3];
+                        for (int r = 0; r < 3; ++r)
+                            vv[r] = A(A(A(M(wv[0], d.view[4 * r]), M(wv[1], d.view[4 * r + 1])),
+                                        M(wv[2], d.view[4 * r + 2])), M(wv[3], d.view[4 * r + 3]));
+                        vx[k] = vv[0]; vy[k] = vv[1]; vz[k] = vv[2];
+                    }
+                    int64_t area;
+                    const int route = debug_route(vx, vy, vz, d.p0, d.p1, d.near, d.width,
+                                                  d.height, d.small_max, d.medium_max, area);
+                    int ci = route;
+                    if (route != 3 && d.mode == 2)
+                        ci = area < d.small_max ? 0 : (area < d.medium_max ? 1 : 2);
+                    for (int q = 0; q < 4; ++q) c[q] = kStageColor[ci][q];
+                }
+            }
+        }
+        o[0] = c[0]; o[1] = c[1]; o[2] = c[2]; o[3] = c[3];
+    }
+}
 }  // namespace
 
 extern "C" {
@@ -283,6 +425,28 @@ int curast_resolve(const curast_resolve_t *r, void *stream) {
     else if (pf == CURAST_POS_F32 && ix == CURAST_IDX_PACKED) k_resolve<1, 1><<<grid, 256, 0, st>>>(*r);
     else if (pf == CURAST_POS_F64 && ix == CURAST_IDX_PACKED) k_resolve<0, 1><<<grid, 256, 0, st>>>(*r);
     else if (pf == CURAST_POS_U16 && ix == CURAST_IDX_PACKED) k_resolve<2, 1><<<grid, 256, 0, st>>>(*r);
+    else return CURAST_E_INVALID;
+    return cudaGetLastError() == cudaSuccess ? 0 : CURAST_E_CUDA;
+}
+
+int curast_debug_view(const curast_debug_t *d, void *stream) {
+    if (!d || !d->fb || !d->out_rgba || d->width <= 0 || d->height <= 0 || d->mode < 0 ||
+        d->mode > 3 || (d->mode == 0 && !d->scratch))
+        return CURAST_E_INVALID;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int grid = sms() * 8;
+    if (d->mode == 0) {
+        const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+        cudaMemcpyAsync(d->scratch, init, sizeof(init), cudaMemcpyHostToDevice, st);
+        k_debug_range<<<grid, 256, 0, st>>>(d->fb, d->width * d->height, d->scratch);
+    }
+    int pf = d->pos_format, ix = d->idx_format;
+    if (pf == CURAST_POS_F32 && ix == CURAST_IDX_U32) k_debug_view<1, 0><<<grid, 256, 0, st>>>(*d);
+    else if (pf == CURAST_POS_F64 && ix == CURAST_IDX_U32) k_debug_view<0, 0><<<grid, 256, 0, st>>>(*d);
+    else if (pf == CURAST_POS_U16 && ix == CURAST_IDX_U32) k_debug_view<2, 0><<<grid, 256, 0, st>>>(*d);
+    else if (pf == CURAST_POS_F32 && ix == CURAST_IDX_PACKED) k_debug_view<1, 1><<<grid, 256, 0, st>>>(*d);
+    else if (pf == CURAST_POS_F64 && ix == CURAST_IDX_PACKED) k_debug_view<0, 1><<<grid, 256, 0, st>>>(*d);
+    else if (pf == CURAST_POS_U16 && ix == CURAST_IDX_PACKED) k_debug_view<2, 1><<<grid, 256, 0, st>>>(*d);
     else return CURAST_E_INVALID;
     return cudaGetLastError() == cudaSuccess ? 0 : CURAST_E_CUDA;
 }

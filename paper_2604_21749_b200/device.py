@@ -37,6 +37,15 @@ U = 2.0 ** -24
 E_FACTOR = {N.POS_F32: 6.0, N.POS_F64: 7.0, N.POS_U16: 10.0}
 
 
+def _to_device(a: np.ndarray, device) -> torch.Tensor:
+    """Host array -> device tensor without a host copy; read-only inputs
+    (e.g. TRIMESH1 payloads viewing the file buffer) are only read."""
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(a).to(device)
+
+
 def _require_cuda():
     if not torch.cuda.is_available():
         raise N.NativeError("no CUDA device: the B200 path has no CPU fallback")
@@ -54,7 +63,7 @@ class DeviceMesh:
         if is_quantized_positions(pos):
             self.pos_format = N.POS_U16
             coords = np.ascontiguousarray(pos.coords, dtype=np.uint16)
-            self.positions = torch.from_numpy(coords.view(np.int16)).to(device)
+            self.positions = _to_device(coords.view(np.int16), device)
             self.qgrid = np.concatenate([np.asarray(pos.grid_min, dtype=np.float64),
                                          np.asarray(pos.grid_size, dtype=np.float64)])
             gmin = np.abs(self.qgrid[:3])
@@ -99,7 +108,7 @@ class DeviceMesh:
         else:
             i32 = np.ascontiguousarray(idx, dtype=np.uint32).ravel()
             self.idx_format = N.IDX_U32
-            self.indices = torch.from_numpy(i32.view(np.int32)).to(device)
+            self.indices = _to_device(i32.view(np.int32), device)
             self.pack = (0, 32)
 
     def positions_as(self, fmt):

@@ -194,3 +194,67 @@ def downsample(image, factor: int):
         raise ValueError("internal resolution must be a multiple of the factor")
     dev = torch.from_numpy(np.ascontiguousarray(img)).cuda()
     return downsample_device(dev, factor).cpu().numpy()
+
+
+_DEBUG_MODES = {"depth": 0, "stageID": 1, "bboxSize": 2, "meshID": 3}
+
+
+def debug_view_device(framebuffer, draw_list, camera, mode: str, cfg=None,
+                      background=(40, 40, 44, 255)) -> torch.Tensor:
+    """Diagnostic views of the visibility buffer on the GPU
+    (resolvepass.py:417-490): 'depth' (log-scaled grey), 'stageID' (the stage
+    whose classification the winning triangle satisfies), 'bboxSize'
+    (green / yellow / red by the bbox-size thresholds), 'meshID'.  Returns a
+    uint8 CUDA tensor [h, w, 4]."""
+    from .config import RasterConfig
+    if mode not in _DEBUG_MODES:
+        raise ValueError(f"unknown debug view mode {mode!r}")
+    cfg = cfg or RasterConfig()
+    L = N.lib()
+    device = torch.device("cuda", torch.cuda.current_device())
+    w, h = framebuffer.width, framebuffer.height
+    words = framebuffer.device_words
+    out = torch.empty((h, w, 4), dtype=torch.uint8, device=device)
+    if draw_list.total_triangles == 0 or len(draw_list.items) == 0:
+        out[:] = torch.tensor(background, dtype=torch.uint8, device=device)
+        return out
+    ctx = build_context(draw_list, camera)
+    geo = scene_geometry(ctx.meshes, device)
+    xform = np.stack([np.asarray(it.instance_transform, dtype=np.float64).reshape(4, 4)
+                      for it in draw_list.items])
+    up = PackedUpload()
+    kp = up.add(ctx.prefix)
+    kvo = up.add(np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64))
+    kio = up.add(np.asarray([geo.idx_off[i] for i in ctx.item_mesh], dtype=np.int64))
+    kq = up.add(np.stack([geo.meshes[i].qgrid for i in ctx.item_mesh]).reshape(-1))
+    kpk = up.add(np.asarray([geo.meshes[i].pack for i in ctx.item_mesh], dtype=np.int64).reshape(-1))
+    kx = up.add(xform.reshape(-1))
+    up.upload(device)
+    scratch = torch.zeros(2, dtype=torch.int32, device=device)
+    d = N.CurastDebug()
+    d.fb = words.data_ptr()
+    d.width, d.height, d.mode = w, h, _DEBUG_MODES[mode]
+    d.pos_format, d.idx_format = geo.pos_format, geo.idx_format
+    d.n_items = len(draw_list.items)
+    d.prefix, d.item_vtx_off, d.item_idx_off = up.ptr(kp), up.ptr(kvo), up.ptr(kio)
+    d.positions, d.indices = geo.positions.data_ptr(), geo.indices.data_ptr()
+    d.item_qgrid, d.item_pack, d.item_xform = up.ptr(kq), up.ptr(kpk), up.ptr(kx)
+    view = np.asarray(camera.view_transform, dtype=np.float64).reshape(-1)
+    for i in range(16):
+        d.view[i] = float(view[i])
+    p = projection_vector(camera)
+    d.p0, d.p1, d.near = float(p[0]), float(p[1]), float(camera.near)
+    d.small_max, d.medium_max = int(cfg.small_max_px), int(cfg.medium_max_px)
+    for i in range(4):
+        d.background[i] = int(background[i])
+    d.out_rgba = out.data_ptr()
+    d.scratch = scratch.data_ptr()
+    N.check(L.curast_debug_view(ctypes.byref(d), torch.cuda.current_stream().cuda_stream),
+            "debug_view")
+    return out
+
+
+def debug_view(framebuffer, draw_list, camera, mode: str, cfg=None,
+               background=(40, 40, 44, 255)) -> np.ndarray:
+    """Drop-in for resolvepass.debug_view: host RGBA8 image [h, w, 4]."""
+    return debug_view_device(framebuffer, draw_list, camera, mode, cfg, background).cpu().numpy()

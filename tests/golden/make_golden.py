@@ -304,3 +304,50 @@ def main_trimesh():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trimesh":
     main_trimesh()
+
+
+def main_debug():
+    """debug_view fixtures: the reference's four diagnostic views of a few
+    golden scenes (rebuilt from the stored arrays with the reference's own
+    types, rendered by the reference)."""
+    trirast, conftest = _import_reference()
+    from trirast.config import RasterConfig
+    from trirast.geomcodec import PackedIndexBuffer, QuantizedPositions
+    from trirast.pipeline import render_frame
+    from trirast.resolvepass import debug_view
+    from trirast.scenecore import Camera, Mesh, SceneNode, build_draw_list
+    import ast
+    out = {}
+    for name in ("classifier", "lantern_off", "compressed_sphere", "tiny_on", "quad48_ss2",
+                 "random2024_000", "random2024_003", "route_130x70"):
+        g = np.load(os.path.join(HERE, f"{name}.npz"))
+        nodes = []
+        for i in range(int(g["n_nodes"])):
+            pos, idx = g[f"node{i}_positions"], g[f"node{i}_indices"]
+            if f"node{i}_q_coords" in g:
+                grid = g[f"node{i}_q_grid"]
+                pos = QuantizedPositions(grid_min=grid[:3].copy(), grid_size=grid[3:].copy(),
+                                         coords=g[f"node{i}_q_coords"])
+            if f"node{i}_p_data" in g:
+                mn, b, cnt = (int(v) for v in g[f"node{i}_p_meta"])
+                idx = PackedIndexBuffer(min_index=mn, bits_per_index=b, count=cnt,
+                                        data=g[f"node{i}_p_data"])
+            mesh = Mesh(positions=pos, indices=idx, triangle_count=int(g[f"node{i}_tricount"]),
+                        aabb=g[f"node{i}_aabb"])
+            nodes.append(SceneNode(mesh=mesh, transforms=list(g[f"node{i}_transforms"])))
+        fovy, aspect, near = (float(v) for v in g["cam_scalars"])
+        w, h, ss = (int(v) for v in g["cam_ints"])
+        cam = Camera(position=g["cam_position"], view_transform=g["cam_view"], fovy=fovy,
+                     aspect=aspect, near=near, image_width=w, image_height=h, supersampling=ss)
+        cfg = RasterConfig(**dict(ast.literal_eval(str(g["cfg_json"]))))
+        fb, _ = render_frame(nodes, cam, cfg)
+        assert np.array_equal(fb.words, g["ref_words"]) or np.array_equal(fb.words, g["frame_words"])
+        dl = build_draw_list(nodes, cam)
+        for mode in ("depth", "stageID", "bboxSize", "meshID"):
+            out[f"{name}__{mode}"] = debug_view(fb, dl, cam, mode, cfg)
+    np.savez_compressed(os.path.join(HERE, "debug_views.npz"), **out)
+    print("wrote debug fixtures", len(out))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "debug":
+    main_debug()

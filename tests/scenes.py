@@ -145,7 +145,7 @@ def load_golden(name):
 def golden_names(prefix=""):
     return sorted(f[:-4] for f in os.listdir(GOLDEN)
                   if f.endswith(".npz") and f.startswith(prefix)
-                  and f not in ("generators.npz", "packing.npz", "trimesh.npz")
+                  and f not in ("generators.npz", "packing.npz", "trimesh.npz", "debug_views.npz")
                   and not f.startswith("resolve_"))
 
 

@@ -162,7 +162,8 @@ def test_c_abi_library_exports_every_header_symbol():
 
 
 @pytest.mark.parametrize("cname,pyname", [("curast_frame_t", "CurastFrame"),
-                                           ("curast_resolve_t", "CurastResolve")])
+                                           ("curast_resolve_t", "CurastResolve"),
+                                           ("curast_debug_t", "CurastDebug")])
 def test_struct_layout_matches_header(tmp_path, cname, pyname):
     """Compile a probe against include/curast.h and compare every field
     offset and the struct size with the ctypes mirror."""
