@@ -105,7 +105,11 @@ def test_queue_autogrow_keeps_output(monkeypatch):
     assert np.array_equal(fb.words, ref)
 
 
-def test_tiny_cull_and_instancing_toggles_bit_identical():
+@pytest.mark.parametrize("inst_kernel", ["0", "1"])
+def test_tiny_cull_and_instancing_toggles_bit_identical(inst_kernel, monkeypatch):
+    """Both stage-1 routes of an instanced frame (the instanced kernel and
+    the flat table over the items, pipeline._instanced_kernel_preferred)."""
+    monkeypatch.setenv("CURAST_INSTANCED_KERNEL", inst_kernel)
     mesh = gen.make_tessellated_quad(300)
     cam = Camera.look_at((0.0, 0.0, 3.2), (0.0, 0.0, 0.0), width=96, height=96)
     scene = [SceneNode(mesh=mesh, transforms=[np.eye(4)])]
