@@ -212,9 +212,7 @@ __global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_
                 ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
                 ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
             } else {
-#pragma unroll
-                for (int k = 0; k < 3 * W_TPL; ++k)
-                    ix[k] = (k < 3 * nv) ? G.index(3 * (lo + o) + k) : 0u;
+                G.template index_run<3 * W_TPL>(3 * (lo + o), 3 * nv, ix);
             }
             float px[3 * W_TPL], py[3 * W_TPL], pz[3 * W_TPL];
 #pragma unroll

@@ -7,7 +7,8 @@ Layout in HBM (per GPU):
     exactly representable in float32 (16 B/vertex: one 128-bit gather per
     vertex, the roofline layout);
     ``float64[V,3]`` otherwise (the reference's ctx.positions);
-    ``uint16[V,3]`` for ``QuantizedPositions`` (decoded in-register).
+    ``uint16[V,4]`` (x, y, z, 0) for ``QuantizedPositions`` (decoded
+    in-register).
   - indices: ``uint32[3T]``, or the bit-packed stream of a
     ``PackedIndexBuffer`` as little-endian 32-bit words (decoded in-register).
 * per-frame descriptors (one pinned H2D copy per frame): global-ID prefix,
@@ -62,12 +63,15 @@ class DeviceMesh:
         self.device = device
         if is_quantized_positions(pos):
             self.pos_format = N.POS_U16
-            coords = np.ascontiguousarray(pos.coords, dtype=np.uint16)
-            self.positions = _to_device(coords.view(np.int16), device)
+            # u16[V][4] (x, y, z, 0): one 64-bit load per vertex in-kernel
+            c3 = np.asarray(pos.coords, dtype=np.uint16).reshape(-1, 3)
+            coords = np.zeros((len(c3), 4), dtype=np.uint16)
+            coords[:, :3] = c3
             self.qgrid = np.concatenate([np.asarray(pos.grid_min, dtype=np.float64),
                                          np.asarray(pos.grid_size, dtype=np.float64)])
             gmin = np.abs(self.qgrid[:3])
             self.pos_bound = gmin + np.abs(self.qgrid[3:])
+            self.positions = _to_device(coords.view(np.int16), device)
             self.vertex_count = len(coords)
             self._host_f64 = None
         elif isinstance(pos, np.ndarray) and pos.dtype == np.float32:
@@ -118,7 +122,7 @@ class DeviceMesh:
         if fmt == N.POS_F64:
             if self.pos_format == N.POS_F32:
                 return self.positions[:, :3].double()
-            q = self.positions.view(torch.int16).to(torch.int32) & 0xFFFF
+            q = self.positions[:, :3].to(torch.int32) & 0xFFFF
             q = q.double()
             g = torch.from_numpy(self.qgrid).to(self.device)
             # grid_min + (q + 0.5) / 65536.0 * grid_size  (geomcodec.py:101)
