@@ -164,7 +164,10 @@ __device__ __forceinline__ int filter_fast2(const FilterPairs &F, const float *v
 // Stage-1 cull filter (split mode producer): every warp claims chunks and
 // appends the triangles it cannot decide to the global fp64 queue with one
 // atomic per 128 triangles (warp prefix sum).
-template <int PF, int IF, int MINB, bool PAIR>
+// WP: the queue entry carries the triangle's positions (POS_U16: the 9 raw
+// u16 grid coordinates in words 0-2; POS_F32: the 9 floats) for
+// k_s1_exact<.., WITHPOS>.
+template <int PF, int IF, int MINB, bool PAIR, bool WP = false>
 __global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_t f) {
     const int lane = threadIdx.x & 31;
     unsigned int n_frustum = 0, n_tiny = 0;
@@ -248,7 +251,27 @@ __global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_
                 while (need) {
                     const int t = __ffs(need) - 1;
                     need &= need - 1;
-                    if (slot < f.qx_cap) f.qx[CURAST_QX_WORDS * slot + CURAST_QX_TAG] = tag + o + t;
+                    if (slot < f.qx_cap) {
+                        int64_t *e = f.qx + CURAST_QX_WORDS * slot;
+                        if (WP && PF == CURAST_POS_U16) {
+                            uint64_t q[9];
+#pragma unroll
+                            for (int v = 0; v < 3; ++v) {
+                                uint32_t a, b, c;
+                                q16_load(G.pos, ix[3 * t + v], a, b, c);
+                                q[3 * v] = a; q[3 * v + 1] = b; q[3 * v + 2] = c;
+                            }
+                            e[0] = (int64_t)(q[0] | q[1] << 16 | q[2] << 32 | q[3] << 48);
+                            e[1] = (int64_t)(q[4] | q[5] << 16 | q[6] << 32 | q[7] << 48);
+                            e[2] = (int64_t)q[8];
+                        } else if (WP && PF == CURAST_POS_F32) {
+                            *(float4 *)e = make_float4(px[3 * t], py[3 * t], pz[3 * t], px[3 * t + 1]);
+                            *(float4 *)(e + 2) = make_float4(py[3 * t + 1], pz[3 * t + 1],
+                                                             px[3 * t + 2], py[3 * t + 2]);
+                            *(float2 *)(e + 4) = make_float2(pz[3 * t + 2], 0.0f);
+                        }
+                        e[CURAST_QX_TAG] = tag + o + t;
+                    }
                     ++slot;
                 }
             }
