@@ -227,7 +227,7 @@ def run_ours(args):
                                  "tiny": st.stage1.culled_tiny,
                                  "fragments": st.fragments},
                        "setup_s": setup_s},
-            "roofline": {"bound": "hbm", "kernel": "stage 1 = k_s1_lean (fp32 cull) + k_s1_exact (fp64 classify+raster)",
+            "roofline": {"bound": "hbm", "kernel": "stage 1 = k_s1_lean_flat (fp32 cull) + k_s1_exact (fp64 classify+raster)",
                          "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / hbm,
                          "algorithmic_bytes_per_launch": s1_bytes,

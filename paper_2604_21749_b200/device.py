@@ -291,10 +291,11 @@ class SceneGeometry:
         else:
             self.positions = torch.cat(pos_parts)
             self.indices = torch.cat(idx_parts)
-        # chunk boxes feed the f32 / u32 stage-1 fast path
+        # chunk boxes feed the chunk-class fast path of the meshlet kernel
         self.cb_off = [0] * len(dms)
         self.chunk_box = None
-        if self.pos_format == N.POS_F32 and self.idx_format == N.IDX_U32:
+        if (self.pos_format == N.POS_F32 and self.idx_format == N.IDX_U32
+                and os.environ.get("CURAST_MESHLETS", "0") == "1"):
             parts, nb = [], 0
             for k, d in enumerate(dms):
                 b = d.chunk_boxes()

@@ -83,7 +83,7 @@ def launches(path):
     h = rows[i]
     per = defaultdict(list)
     for r in rows[i + 1:]:
-        if len(r) > h.index("Metric Value"):
+        if len(r) > h.index("Metric Value") and r[h.index("Metric Name")] == "gpu__time_duration.sum":
             per[r[h.index("Kernel Name")]].append(float(r[h.index("Metric Value")]))
     tot = sum(sum(v) for v in per.values())
     print(f"{'kernel':70s} {'n':>4s} {'mean ns':>12s} {'share':>7s}")
