@@ -125,6 +125,15 @@ typedef struct curast_frame {
     const int64_t *ml_voff;           /* int64[n_meshlets+1] into ml_verts    */
     const uint32_t *ml_verts;         /* mesh-local vertex ids                */
     const uint8_t *ml_tris;           /* uint8[n_meshlets][CURAST_MESHLET_BYTES] */
+    /* ---- lane-major index steps (POS_F32 + IDX_U32; optional) ----
+     * the u32 stream re-laid out per step of CURAST_MESHLET_TRIS triangles:
+     * 384 words, lane l's 12 words = triangles l, l+32, l+64, l+96 of the
+     * step (3 indices each, zero padded past the step).  One 3 x 128-bit
+     * load per lane, and each vertex gather of the warp then reads 32
+     * consecutive triangles' vertices (fewer L1 lines than 4 consecutive
+     * triangles per lane).                                                  */
+    const int64_t *item_ilv_off;      /* word offset of the item's mesh       */
+    const uint32_t *indices_ilv;
     /* ---- per-chunk object-space boxes (POS_F32 + IDX_U32; optional) ----
      * box b of a mesh bounds the vertices of its triangles
      * [b*C, (b+1)*C), C = curast_chunk_tris(0): float[8] = min xyz, 0,

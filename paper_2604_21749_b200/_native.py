@@ -45,6 +45,7 @@ class CurastFrame(ctypes.Structure):
         ("item_vtx_off", _P), ("item_idx_off", _P), ("item_filter", _P),
         ("item_qgrid", _P), ("item_pack", _P),
         ("item_ml_off", _P), ("ml_voff", _P), ("ml_verts", _P), ("ml_tris", _P),
+        ("item_ilv_off", _P), ("indices_ilv", _P),
         ("item_cb_off", _P), ("chunk_box", _P),
         ("instanced", _I32), ("use_filter", _I32),
         ("n_groups", _I64), ("group_prefix", _P), ("group_item_off", _P),

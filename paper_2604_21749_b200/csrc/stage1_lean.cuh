@@ -458,6 +458,104 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
     flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
 }
 
+// Per-triangle lean kernel over the lane-major index steps (indices_ilv):
+// the same per-triangle work as k_s1_lean_flat, but lane l owns triangles
+// l, l+32, l+64, l+96 of a 126-triangle step, so each of the 12 vertex
+// gathers of a warp reads the vertices of 32 consecutive triangles — about
+// half the L1 lines (the filter is bound by L1 data-pipe wavefronts).
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_s1_lean_ilv(const curast_frame_t f, int64_t cbeg,
+                                                           int64_t cend, int claim_slot) {
+    constexpr int CHUNK = kS1Chunk, MT = CURAST_MESHLET_TRIS, SW = 384;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    unsigned n_frustum = 0, n_tiny = 0;
+    const float W = (float)f.width, H = (float)f.height;
+    const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
+    const bool tiny = f.tiny_cull != 0;
+    const int64_t total = min(cend, __ldg(f.unit_chunk_prefix + f.n_units));
+    unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+    for (;;) {
+        long long c = 0, item = 0, lo = 0, hi = 0;
+        if (lane == 0) {
+            c = cbeg + (long long)atomicAdd((unsigned long long *)(f.counters + claim_slot), 1ull);
+            if (c < total) {
+                const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
+                item = __ldg(f.unit_index + u);
+                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * CHUNK;
+                hi = __ldg(f.unit_hi + u);
+                hi = lo + CHUNK < hi ? lo + CHUNK : hi;
+            }
+        }
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= total) break;
+        item = __shfl_sync(0xffffffffu, item, 0);
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        hi = __shfl_sync(0xffffffffu, hi, 0);
+
+        LeanConsts F;
+        lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);
+        const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + item);
+        // chunk-relative 32-bit triangle numbers from the first step it touches
+        const long long s0 = lo / MT, base = s0 * MT;
+        const int rlo = (int)(lo - base), rhi = (int)(hi - base);
+        const uint4 *sp = (const uint4 *)(f.indices_ilv + __ldg(f.item_ilv_off + item) + s0 * SW);
+        const long long tag = (item << 40) | base;
+        const int nst = (rhi + MT - 1) / MT;
+        for (int st = 0; st < nst; ++st) {
+            const uint4 *v = sp + st * (SW / 4) + 3 * lane;
+            const uint4 a = __ldg(v), b4 = __ldg(v + 1), d = __ldg(v + 2);
+            const uint32_t ix[12] = {a.x, a.y, a.z, a.w, b4.x, b4.y, b4.z, b4.w, d.x, d.y, d.z, d.w};
+            const int tb = st * MT + lane;            // slot t: tb + 32 t
+            const int lim = min(rhi, st * MT + MT);
+            unsigned valid = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) valid |= (unsigned)(tb + 32 * t >= rlo && tb + 32 * t < lim) << t;
+            float px[12], py[12], pz[12];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) {
+                const float4 q = __ldg(pb + ix[k]);
+                px[k] = q.x;
+                py[k] = q.y;
+                pz[k] = q.z;
+            }
+            unsigned need = 0, fr = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const unsigned bits = lean_bits(F, px + 3 * t, py + 3 * t, pz + 3 * t, W, H, slack, tiny);
+                need |= (bits & 1u) << t;
+                fr |= (bits >> 1) << t;
+            }
+            need &= valid;
+            fr &= valid;
+            n_frustum += __popc(fr);
+            n_tiny += __popc(valid) - __popc(need) - __popc(fr);
+            unsigned b[4];
+            int tot = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                b[t] = __ballot_sync(0xffffffffu, (need >> t) & 1u);
+                tot += __popc(b[t]);
+            }
+            if (tot) {
+                unsigned long long qb = 0;
+                if (lane == 0) qb = atomicAdd(qcount, (unsigned long long)tot);
+                qb = __shfl_sync(0xffffffffu, qb, 0);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if ((need >> t) & 1u)
+                        qx_write(f, (long long)qb + __popc(b[t] & lt_mask), px + 3 * t, py + 3 * t,
+                                 pz + 3 * t, tag + tb + 32 * t);
+                    qb += __popc(b[t]);
+                }
+            }
+        }
+    }
+    unsigned long long cnt[2] = {n_frustum, n_tiny};
+    flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+    flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+}
+
 // Meshlet lean kernel (flat table, meshes with meshlets; CURAST_MESHLETS=1).
 // Per batch of triangles a warp
 //   1. gathers and projects each listed vertex once (lanes j, j+32, ...; the

@@ -136,6 +136,12 @@ class DeviceMesh:
             self._meshlets = build_meshlets(self.indices_u32(), self.triangle_count)
         return self._meshlets
 
+    def index_steps(self):
+        """Lane-major index steps of the u32 stream (built once)."""
+        if getattr(self, "_index_steps", None) is None:
+            self._index_steps = build_index_steps(self.indices_u32(), self.triangle_count)
+        return self._index_steps
+
     def chunk_boxes(self):
         """Per-chunk object-space boxes (POS_F32 meshes), built once."""
         if getattr(self, "_chunk_boxes", None) is None:
@@ -197,6 +203,23 @@ def build_meshlets(indices: torch.Tensor, triangle_count: int, block: int = 1 <<
     voff = torch.zeros(nm + 1, dtype=torch.int64, device=dev)
     voff[1:] = torch.cumsum(nu, 0)
     return voff, torch.cat(verts), torch.cat(tris)
+
+
+def build_index_steps(indices: torch.Tensor, triangle_count: int) -> torch.Tensor:
+    """Lane-major index steps (curast.h indices_ilv): per step of MT
+    triangles 384 words, lane l holding triangles l + 32k (k < 4, zero padded
+    past the step) as 3 consecutive indices each."""
+    MT = N.MESHLET_TRIS
+    T = int(triangle_count)
+    ns = -(-T // MT)
+    dev = indices.device
+    if ns == 0:
+        return torch.zeros(0, dtype=torch.int32, device=dev)
+    x = torch.zeros((ns * MT, 3), dtype=torch.int32, device=dev)
+    x[:T] = indices[:3 * T].view(T, 3)
+    x = torch.cat([x.view(ns, MT, 3), torch.zeros((ns, 128 - MT, 3), dtype=torch.int32,
+                                                  device=dev)], dim=1)
+    return x.view(ns, 4, 32, 3).permute(0, 2, 1, 3).contiguous().view(-1)
 
 
 def build_chunk_boxes(pos4: torch.Tensor, indices: torch.Tensor, triangle_count: int,
@@ -291,6 +314,9 @@ class SceneGeometry:
         else:
             self.positions = torch.cat(pos_parts)
             self.indices = torch.cat(idx_parts)
+        # lane-major index steps (built on first use, SceneGeometry.index_steps)
+        self.ilv_off = [0] * len(dms)
+        self.indices_ilv = None
         # chunk boxes feed the chunk-class fast path of the meshlet kernel
         self.cb_off = [0] * len(dms)
         self.chunk_box = None
@@ -324,6 +350,20 @@ class SceneGeometry:
             self.ml_verts = vt_parts[0] if len(vt_parts) == 1 else torch.cat(vt_parts)
             self.ml_tris = tr_parts[0] if len(tr_parts) == 1 else torch.cat(tr_parts)
         self.keepalive = dms
+
+    def index_steps(self):
+        """Lane-major index steps of every mesh (curast.h indices_ilv) for the
+        f32 / u32 per-triangle kernel; None for other formats."""
+        if self.indices_ilv is None and self.pos_format == N.POS_F32 \
+                and self.idx_format == N.IDX_U32:
+            parts, nw = [], 0
+            for k, d in enumerate(self.meshes):
+                st = d.index_steps()
+                self.ilv_off[k] = nw
+                parts.append(st)
+                nw += st.numel()
+            self.indices_ilv = parts[0] if len(parts) == 1 else torch.cat(parts)
+        return self.indices_ilv
 
 
 _scene_cache: dict = {}

@@ -60,3 +60,9 @@ def test_switch_is_bit_exact(env):
     r = subprocess.run([sys.executable, "-c", script], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [{"CURAST_ILV": "1"}, {"CURAST_ILV": "0"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_index_step_layout_is_bit_exact(env):
+    test_switch_is_bit_exact(env)
