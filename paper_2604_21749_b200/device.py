@@ -47,6 +47,13 @@ def _to_device(a: np.ndarray, device) -> torch.Tensor:
         return torch.from_numpy(a).to(device)
 
 
+def _pad4(p3: torch.Tensor) -> torch.Tensor:
+    """(V, 3) -> (V, 4) with a zero pad column, on p3's device."""
+    p4 = torch.zeros((p3.shape[0], 4), dtype=p3.dtype, device=p3.device)
+    p4[:, :3] = p3
+    return p4
+
+
 def _require_cuda():
     if not torch.cuda.is_available():
         raise N.NativeError("no CUDA device: the B200 path has no CPU fallback")
@@ -75,32 +82,33 @@ class DeviceMesh:
             self.vertex_count = len(coords)
             self._host_f64 = None
         elif isinstance(pos, np.ndarray) and pos.dtype == np.float32:
-            # stored f32 (e.g. a TRIMESH1 payload): exact by construction
-            p32 = pos.reshape(-1, 3)
-            self.vertex_count = len(p32)
+            # stored f32 (e.g. a TRIMESH1 payload): exact by construction;
+            # uploaded as is, padded to float4 on the device
+            d32 = _to_device(np.ascontiguousarray(pos.reshape(-1, 3)), device)
+            self.vertex_count = int(d32.shape[0])
             self.qgrid = np.zeros(6)
-            self.pos_bound = (np.abs(p32).max(axis=0).astype(np.float64) if len(p32)
+            self.pos_bound = (d32.abs().amax(dim=0).double().cpu().numpy() if self.vertex_count
                               else np.zeros(3))
             self.pos_format = N.POS_F32
-            p4 = np.zeros((len(p32), 4), dtype=np.float32)
-            p4[:, :3] = p32
-            self.positions = torch.from_numpy(p4).to(device)
+            self.positions = _pad4(d32)
         else:
+            # f64 positions: uploaded once, the f32-exactness check and the
+            # float4 packing run on the device (one host pass fewer per array)
             p64 = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
-            p32 = p64.astype(np.float32)
+            d64 = _to_device(p64, device)
             self.vertex_count = len(p64)
             self.qgrid = np.zeros(6)
-            self.pos_bound = (np.abs(p64).max(axis=0) if len(p64) else np.zeros(3))
-            if np.array_equal(p32.astype(np.float64), p64):
+            self.pos_bound = (d64.abs().amax(dim=0).cpu().numpy() if len(p64) else np.zeros(3))
+            d32 = d64.float()
+            if torch.equal(d32.double(), d64):
                 # float4 per vertex: a stage-1 vertex gather is one 128-bit
                 # load; the pad word is never read as data
                 self.pos_format = N.POS_F32
-                p4 = np.zeros((len(p32), 4), dtype=np.float32)
-                p4[:, :3] = p32
-                self.positions = torch.from_numpy(p4).to(device)
+                self.positions = _pad4(d32)
+                del d64
             else:
                 self.pos_format = N.POS_F64
-                self.positions = torch.from_numpy(p64).to(device)
+                self.positions = d64
         if is_packed_indices(idx):
             self.idx_format = N.IDX_PACKED
             data = np.asarray(idx.data, dtype=np.uint8)
