@@ -247,8 +247,11 @@ typedef struct curast_resolve {
     double p0, p1;
     double cam[3];
     double rot[9];                    /* view_transform[:3,:3] (row-major)     */
-    uint8_t *out_rgba;                /* uint8[height*width*4]                 */
+    uint8_t *out_rgba;                /* uint8[rows*width*4]                   */
     int64_t *counters;                /* [0] shaded [1] background [2] degenerate */
+    /* image rows [row0, row0 + rows) only (a sort-last stripe): fb and
+     * out_rgba point at row row0; rows = 0 means the whole image         */
+    int64_t row0, rows;
 } curast_resolve_t;
 
 int curast_resolve(const curast_resolve_t *r, void *stream);

@@ -89,7 +89,7 @@ class CurastResolve(ctypes.Structure):
         ("trilinear", _I32), ("headlight", _I32),
         ("background", ctypes.c_uint8 * 4), ("base_color", ctypes.c_uint8 * 4),
         ("p0", _D), ("p1", _D), ("cam", _D * 3), ("rot", _D * 9),
-        ("out_rgba", _P), ("counters", _P),
+        ("out_rgba", _P), ("counters", _P), ("row0", _I64), ("rows", _I64),
     ]
 
 

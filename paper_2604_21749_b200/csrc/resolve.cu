@@ -100,7 +100,7 @@ __global__ void k_resolve(const curast_resolve_t r) {
     __syncthreads();
     const curast_frame_t f = geo_view(r);
     unsigned long long shaded = 0, bg = 0, degen = 0;
-    const int64_t npix = r.width * r.height;
+    const int64_t npix = r.width * (r.rows > 0 ? r.rows : r.height);
     for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < npix;
          pix += (int64_t)gridDim.x * blockDim.x) {
         uint64_t word = r.fb[pix];
@@ -130,7 +130,7 @@ __global__ void k_resolve(const curast_resolve_t r) {
             w[k] = v3(x * m[0] + y * m[1] + z * m[2] + m[3], x * m[4] + y * m[5] + z * m[6] + m[7],
                       x * m[8] + y * m[9] + z * m[10] + m[11]);
         }
-        const double xs = (double)(pix % r.width), ys = (double)(pix / r.width);
+        const double xs = (double)(pix % r.width), ys = (double)(r.row0 + pix / r.width);
         const V3 dir = pixel_dir(r, xs, ys);
         const V3 org = v3(r.cam[0], r.cam[1], r.cam[2]);
         // _moller_trumbore_bulk (resolvepass.py:184-205)
@@ -414,7 +414,8 @@ __global__ void k_debug_view(const curast_debug_t d) {
 extern "C" {
 
 int curast_resolve(const curast_resolve_t *r, void *stream) {
-    if (!r || !r->fb || !r->out_rgba || !r->counters || r->width <= 0 || r->height <= 0)
+    if (!r || !r->fb || !r->out_rgba || !r->counters || r->width <= 0 || r->height <= 0 ||
+        r->row0 < 0 || r->rows < 0 || r->row0 + r->rows > r->height)
         return CURAST_E_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     int grid = sms() * 8;

@@ -159,3 +159,64 @@ def render_sharded(draw_list, camera, cfg=None, *, group=None):
         comp = Compositor(pf.fb, world)
         comp.allreduce_min()
     return Framebuffer(camera.internal_width, camera.internal_height, device_words=pf.fb), st
+
+
+def stripe_rows(height: int, world: int, rank: int) -> tuple[int, int, int]:
+    """(first row, rows, rows per stripe) of ``rank``'s resolve stripe: equal
+    stripes of ceil(H / world) rows (NCCL reduce-scatter needs equal
+    counts; the tail is padded with CLEAR rows)."""
+    per = -(-int(height) // int(world))
+    r0 = int(rank) * per
+    return r0, max(0, min(per, int(height) - r0)), per
+
+
+def render_sharded_resolved(draw_list, camera, cfg=None, shading=None, *, root=0, group=None):
+    """Sort-last frame with a striped resolve: rasterize this
+    rank's shard, reduce-scatter the visibility buffers by unsigned min so
+    each rank owns a stripe of rows, shade the stripe
+    (resolve_frame_device(rows=...)), gather the RGBA8 stripes on ``root``.
+    Returns (image [H, W, 4] uint8 CUDA tensor on root / None elsewhere,
+    this rank's FrameStats, this rank's ResolveStats)."""
+    from .config import RasterConfig, ShadingConfig
+    from .pipeline import PreparedFrame, build_context
+    from .resolve import resolve_frame_device
+    from .scene import Framebuffer
+    cfg = cfg or RasterConfig()
+    shading = shading or ShadingConfig()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ctx = build_context(draw_list, camera)
+    instanced = (cfg.instancing == "on"
+                 or (cfg.instancing == "auto" and ctx.max_instances >= 2))
+    space = int(ctx.group_prefix[-1]) if instanced else int(draw_list.total_triangles)
+    lo, hi = shard_range(space, world, rank)
+    pf = PreparedFrame(draw_list, camera, cfg, ctx, work_range=(lo, hi))
+    c, secs = pf.run()
+    st = pf.stats(c, secs)
+    W, H = camera.internal_width, camera.internal_height
+    r0, n, per = stripe_rows(H, world, rank)
+    words = pf.fb
+    if per * world * W > words.numel():                    # pad with CLEAR rows
+        words = torch.cat([words, words.new_full((per * world * W - words.numel(),), -1)])
+    stripe = torch.empty(per * W, dtype=torch.int64, device=words.device)
+    if world > 1 and words.is_cuda and dist.get_backend(group) == "nccl" and os.path.exists(NCCL_LIB):
+        comm = NcclComm(group)
+        comm.reduce_scatter_min(words, stripe)
+        comm.close()
+    else:
+        full = words.clone()
+        if world > 1:
+            composite_min_u64_(full, group)
+        stripe.copy_(full[rank * per * W:(rank + 1) * per * W])
+    fb = Framebuffer(W, H, device_words=pf.fb)
+    img, rst = resolve_frame_device(fb, draw_list, camera, shading, rows=(r0, n),
+                                    stripe_words=stripe[:n * W])
+    part = torch.zeros((per, W, 4), dtype=torch.uint8, device=img.device)
+    part[:n] = img
+    if world > 1:
+        parts = [torch.empty_like(part) for _ in range(world)]
+        dist.all_gather(parts, part, group=group)
+    else:
+        parts = [part]
+    image = torch.cat(parts)[:H] if rank == root else None
+    return image, st, rst

@@ -96,21 +96,30 @@ def _attributes(meshes, geo, device):
     return a
 
 
-def resolve_frame_device(framebuffer, draw_list, camera, shading: ShadingConfig | None = None):
+def resolve_frame_device(framebuffer, draw_list, camera, shading: ShadingConfig | None = None,
+                         *, rows=None, stripe_words=None):
     """Shade every pixel on the GPU; returns (uint8 CUDA tensor [h, w, 4],
-    ResolveStats)."""
+    ResolveStats).  ``rows=(row0, n)`` shades image rows [row0, row0 + n)
+    only (a sort-last stripe) from ``stripe_words`` (int64 CUDA tensor of
+    n*w words; default: the framebuffer's rows) into an [n, w, 4] image."""
     L = N.lib()
     shading = shading or ShadingConfig()
     device = torch.device("cuda", torch.cuda.current_device())
     w, h = framebuffer.width, framebuffer.height
-    words = framebuffer.device_words if hasattr(framebuffer, "device_words") else \
-        torch.from_numpy(np.asarray(framebuffer.words).view(np.int64).copy()).to(device)
-    out = torch.empty((h, w, 4), dtype=torch.uint8, device=device)
+    if stripe_words is not None:
+        words = stripe_words
+    else:
+        words = framebuffer.device_words if hasattr(framebuffer, "device_words") else \
+            torch.from_numpy(np.asarray(framebuffer.words).view(np.int64).copy()).to(device)
+    row0, nrows = (0, h) if rows is None else (int(rows[0]), int(rows[1]))
+    if stripe_words is None and rows is not None:
+        words = words[row0 * w:(row0 + nrows) * w]
+    out = torch.empty((nrows, w, 4), dtype=torch.uint8, device=device)
     counters = torch.zeros(4, dtype=torch.int64, device=device)
     st = ResolveStats()
     if draw_list.total_triangles == 0 or len(draw_list.items) == 0:
         out[:] = torch.tensor(shading.background, dtype=torch.uint8, device=device)
-        st.background = w * h
+        st.background = w * nrows
         return out, st
     ctx = build_context(draw_list, camera)
     geo = scene_geometry(ctx.meshes, device)
@@ -156,6 +165,7 @@ def resolve_frame_device(framebuffer, draw_list, camera, shading: ShadingConfig 
         r.rot[i] = float(rot[i])
     r.out_rgba = out.data_ptr()
     r.counters = counters.data_ptr()
+    r.row0, r.rows = row0, nrows
     N.check(L.curast_resolve(ctypes.byref(r), torch.cuda.current_stream().cuda_stream),
             "resolve")
     c = counters.cpu().numpy()

@@ -61,3 +61,16 @@ def test_render_sharded_equals_render_frame(nccl_group):
         fb1, _ = cr.render_frame(scene, cam, cr.RasterConfig())
         fb2, _ = render_sharded(dl, cam, cr.RasterConfig())
         assert np.array_equal(fb1.words, fb2.words)
+
+
+def test_render_sharded_resolved_equals_single_gpu(nccl_group):
+    import paper_2604_21749_b200 as cr
+    from paper_2604_21749_b200 import generators as gen
+    from paper_2604_21749_b200.distributed import render_sharded_resolved
+    from paper_2604_21749_b200.resolve import resolve_frame_device
+    scene, cam = gen.config_a()
+    dl = cr.build_draw_list(scene, cam)
+    img, st, rst = render_sharded_resolved(dl, cam, group=nccl_group)
+    fb, _ = cr.render_draw_list(dl, cam)
+    ref, _ = resolve_frame_device(fb, dl, cam)
+    assert img is not None and torch.equal(img, ref)

@@ -86,3 +86,25 @@ def test_downsample_box_properties():
             assert np.array_equal(out, (blocks.sum(axis=(1, 3)) // (f * f)).astype(np.uint8))
     with pytest.raises(ValueError):
         downsample(np.zeros((6, 8, 4), dtype=np.uint8), 4)
+
+
+def test_striped_resolve_equals_full_resolve():
+    """resolve_frame_device(rows=...) shades exactly the rows of the full
+    image (the sort-last stripe path)."""
+    import torch
+    from paper_2604_21749_b200.resolve import resolve_frame_device
+    from paper_2604_21749_b200.distributed import stripe_rows
+    from paper_2604_21749_b200 import generators as gen
+    from paper_2604_21749_b200 import render_draw_list
+    scene, cam = gen.config_a()
+    dl = build_draw_list(scene, cam)
+    fb, _ = render_draw_list(dl, cam)
+    full, _ = resolve_frame_device(fb, dl, cam)
+    H = cam.internal_height
+    for world in (2, 3):
+        parts = []
+        for r in range(world):
+            r0, n, _ = stripe_rows(H, world, r)
+            img, _ = resolve_frame_device(fb, dl, cam, rows=(r0, n))
+            parts.append(img)
+        assert torch.equal(torch.cat(parts), full)

@@ -100,3 +100,15 @@ def test_sign_flip_min_is_unsigned_min():
     u ^= -0x8000000000000000
     m = torch.minimum(t, u) ^ -0x8000000000000000
     assert np.array_equal(m.numpy().view(np.uint64), np.minimum(a, b))
+
+
+def test_stripe_rows_cover_the_image_once():
+    from paper_2604_21749_b200.distributed import stripe_rows
+    for H in (1, 7, 120, 1080, 2160):
+        for world in (1, 2, 3, 4, 8):
+            rows = []
+            for r in range(world):
+                r0, n, per = stripe_rows(H, world, r)
+                assert per * world >= H and n <= per
+                rows += list(range(r0, r0 + n))
+            assert rows == list(range(H))
