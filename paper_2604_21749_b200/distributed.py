@@ -136,6 +136,27 @@ class Compositor:
         else:
             composite_min_u64_(self.words)
 
+    def reduce_scatter_min(self, rank: int):
+        """Composite into stripes: this rank receives the unsigned-min of all
+        ranks' words over its 1/world slice (self.stripe); the full VB exists
+        once, distributed — the input of the striped resolve."""
+        n = self.words.numel()
+        per = -(-n // self.world)
+        if not hasattr(self, "stripe"):
+            self.stripe = torch.empty(per, dtype=torch.int64, device=self.words.device)
+            self._padded = (self.words if per * self.world == n else
+                            torch.full((per * self.world,), -1, dtype=torch.int64,
+                                       device=self.words.device))
+        if self._padded is not self.words:
+            self._padded[:n].copy_(self.words)
+        if self.comm is not None:
+            self.comm.reduce_scatter_min(self._padded, self.stripe)
+        else:
+            full = self._padded.clone()
+            composite_min_u64_(full)
+            self.stripe.copy_(full[rank * per:(rank + 1) * per])
+        return self.stripe
+
 
 def render_sharded(draw_list, camera, cfg=None, *, group=None):
     """Sort-last frame on the calling rank's GPU: rasterize this rank's

@@ -112,3 +112,41 @@ def test_stripe_rows_cover_the_image_once():
                 assert per * world >= H and n <= per
                 rows += list(range(r0, r0 + n))
             assert rows == list(range(H))
+
+
+def _rs_worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_21749_b200.distributed import Compositor
+    try:
+        rng = np.random.default_rng(100 + rank)
+        n = 1001                                   # not a multiple of the world size
+        w = rng.integers(0, 2 ** 63, size=n, dtype=np.int64)
+        w[::7] = -1                                # CLEAR words (all ones)
+        w[::11] = np.int64(-2 ** 63)               # top bit set: unsigned order != signed
+        t = torch.from_numpy(w.copy())
+        stripe = Compositor(t, world).reduce_scatter_min(rank).clone()
+        allw = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allw, t)
+        parts = [torch.empty_like(stripe) for _ in range(world)]
+        dist.all_gather(parts, stripe)
+        if rank == 0:
+            results["words"] = np.stack([a.numpy() for a in allw])
+            results["stripes"] = torch.cat(parts).numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reduce_scatter_stripes_are_the_unsigned_min():
+    """Compositor.reduce_scatter_min (the bench's sort-last composite): the
+    concatenated stripes equal the elementwise unsigned min of all ranks'
+    words, CLEAR-padded to equal stripes."""
+    world = 2
+    results = mp.Manager().dict()
+    mp.spawn(_rs_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    words = results["words"].view(np.uint64)
+    want = words.min(axis=0)
+    got = results["stripes"].view(np.uint64)
+    assert np.array_equal(got[:len(want)], want)
+    assert np.all(got[len(want):] == np.uint64(2 ** 64 - 1))
