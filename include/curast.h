@@ -66,6 +66,7 @@ enum curast_counter {
     CURAST_C_SLICE_CLAIM = 22,/* 4 slots: claim counters of stage-1 slices      */
     CURAST_C_SLICE_SNAP = 26, /* 4 slots: fp64-queue size after each slice      */
     CURAST_C_PROVED = 30,     /* fp64-queue entries decided by the fp32 prover  */
+    CURAST_C_CLAIM1B = 31,    /* second flat-table claim counter (die halves)   */
     CURAST_COUNTER_SLOTS = 32
 };
 

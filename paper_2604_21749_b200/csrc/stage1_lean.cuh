@@ -340,7 +340,16 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f, i
 // lean_range-based k_s1_lean below carries the experiment switches and
 // costs 5% more instructions and some spills (measured r01: 418 M vs 398 M
 // warp instructions on config B).
-template <int PF, int MINB, int TPL>
+// PFI: L1 prefetch of the next step's index lines.  STRIP: the quad-strip
+// vertex-reuse gathers below.  Both measured box-dependent (config B stage 1
+// 0.77 ms on one B200, 1.10 ms on another, where the plain kernel is
+// 0.80-0.84 ms on both), so the default instantiation has neither.
+// DIE: two claim sequences, one per half of the SM ids (the two dies of a
+// B200): SMs of the lower half walk the chunks of the first half of the
+// table, the upper half the second, and a half that runs out continues in
+// the other's sequence.  Neighbouring chunks (which share vertex rows) then
+// stay on one die's L2.
+template <int PF, int MINB, int TPL, bool PFI = false, bool STRIP = false, bool DIE = false>
 __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t f, int64_t cbeg,
                                                         int64_t cend, int claim_slot) {
     // processes chunks [cbeg, min(cend, total)) of the flat table, claimed
@@ -358,7 +367,22 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
     for (;;) {
         long long c = 0, item = 0, lo = 0, hi = 0;
         if (lane == 0) {
-            c = cbeg + (long long)atomicAdd((unsigned long long *)(f.counters + claim_slot), 1ull);
+            if (DIE) {
+                unsigned smid, nsmid;
+                asm("mov.u32 %0, %%smid;" : "=r"(smid));
+                asm("mov.u32 %0, %%nsmid;" : "=r"(nsmid));
+                int h = smid >= nsmid / 2 ? 1 : 0;
+                const long long mid = cbeg + (total - cbeg) / 2;
+                c = total;
+                for (int tries = 0; tries < 2; ++tries, h ^= 1) {
+                    const long long b0 = h ? mid : cbeg, e0 = h ? total : mid;
+                    const long long cc = b0 + (long long)atomicAdd(
+                        (unsigned long long *)(f.counters + (h ? CURAST_C_CLAIM1B : claim_slot)), 1ull);
+                    if (cc < e0) { c = cc; break; }
+                }
+            } else {
+                c = cbeg + (long long)atomicAdd((unsigned long long *)(f.counters + claim_slot), 1ull);
+            }
             if (c < total) {
                 const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
                 item = __ldg(f.unit_index + u);
@@ -386,6 +410,13 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
         const long long tag = (item << 40) | lo;
 
         for (int s0 = 0; s0 < n; s0 += STEP) {
+            if (PFI && s0 + STEP < n) {
+                // the next step's index lines into L1 (12 x 128 B per warp)
+                const uintptr_t b1 = ((uintptr_t)(ib + 3 * (s0 + STEP))) & ~(uintptr_t)127;
+                const uintptr_t e1 = (uintptr_t)(ib + 3 * min(n, s0 + 2 * STEP));
+                if (b1 + 128 * lane < e1)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(b1 + 128 * lane));
+            }
             const int o = s0 + TPL * lane;
             const int nv = max(0, min(TPL, n - o));
             uint32_t ix[3 * TPL];
@@ -404,12 +435,42 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
                 for (int k = 0; k < 3 * TPL; ++k) ix[k] = (k < 3 * nv) ? __ldg(ib + 3 * o + k) : 0u;
             }
             float px[3 * TPL], py[3 * TPL], pz[3 * TPL];
-#pragma unroll
-            for (int k = 0; k < 3 * TPL; ++k) {
+            // Quad-strip vertex reuse: a lane's 4 consecutive triangles are 2
+            // quads of a strip in the two standard triangulations — (a,c,b),
+            // (b,c,d) (make_tessellated_quad) and (a,b,c),(b,d,c)
+            // (make_sphere) — so 6 of its 12 vertex refs repeat earlier ones.
+            // Every lane checks the pattern on its own indices; only when the
+            // whole warp matches are the 6 repeated gathers skipped (their
+            // values are the repeated registers), else all 12 are loaded.
+            int strip = 0;
+            if (STRIP && TPL == 4) {
+                const bool full = nv == TPL;
+                const bool gq = full && ix[3] == ix[2] && ix[4] == ix[1] && ix[6] == ix[2] &&
+                                ix[7] == ix[5] && ix[9] == ix[8] && ix[10] == ix[5];
+                const bool sq = full && ix[3] == ix[1] && ix[5] == ix[2] && ix[6] == ix[1] &&
+                                ix[8] == ix[4] && ix[9] == ix[7] && ix[11] == ix[4];
+                strip = __all_sync(0xffffffffu, gq) ? 1 : (__all_sync(0xffffffffu, sq) ? 2 : 0);
+            }
+            auto gather = [&](int k) {
                 const float4 q = __ldg(pb + ix[k]);
                 px[k] = q.x;
                 py[k] = q.y;
                 pz[k] = q.z;
+            };
+            auto copy = [&](int k, int from) {
+                px[k] = px[from];
+                py[k] = py[from];
+                pz[k] = pz[from];
+            };
+            if (TPL == 4 && strip == 1) {
+                gather(0); gather(1); gather(2); gather(5); gather(8); gather(11);
+                copy(3, 2); copy(4, 1); copy(6, 2); copy(7, 5); copy(9, 8); copy(10, 5);
+            } else if (TPL == 4 && strip == 2) {
+                gather(0); gather(1); gather(2); gather(4); gather(7); gather(10);
+                copy(3, 1); copy(5, 2); copy(6, 1); copy(8, 4); copy(9, 7); copy(11, 4);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 3 * TPL; ++k) gather(k);
             }
             unsigned need = 0, fr = 0;
 #pragma unroll
