@@ -56,6 +56,7 @@ sys.exit(1 if bad else 0)
     {"CURAST_INSTANCED_KERNEL": "1"},
     {"CURAST_S1": "strip"},
     {"CURAST_S1": "die"},
+    {"CURAST_S1": "fused", "CURAST_XMINB": "4"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_switch_is_bit_exact(env):
     script = SCRIPT % {"root": ROOT, "tests": os.path.join(ROOT, "tests")}
