@@ -384,6 +384,25 @@ class PreparedFrame:
         if events:
             events[4].record()
 
+    def capture(self):
+        """Capture clear + stages 1-3 into a CUDA graph (torch.cuda.CUDAGraph)
+        for repeated frames of the same draw list: one graph launch per frame
+        instead of five kernel launches through ctypes.  Run the frame once
+        first (``run()``) so the device queues are sized; replay with
+        ``graph.replay()`` and read the counters as after ``launch``.  The
+        graph keeps this frame's device pointers: re-capture after
+        ``_size_queues`` grows a queue."""
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.launch(stream=s)                 # warm the launch path outside capture
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.graph(g):
+            self.launch()
+        return g
+
     def read_counters(self) -> np.ndarray:
         ws = self.ws
         ws.counters_host.copy_(ws.counters, non_blocking=True)
