@@ -72,6 +72,23 @@ class ClockSampler:
         except Exception:
             self.max = None
         self._stop = threading.Event()
+        self.temps = {}
+
+    def _thermals(self, tag):
+        # GPU / HBM temperature and board power around the timed region (the
+        # filter kernel is latency-bound; its run-to-run modes are compared
+        # against these in DESIGN.md)
+        nv = self.nv
+        try:
+            self.temps[f"gpu_temp_c_{tag}"] = int(nv.nvmlDeviceGetTemperature(self.h, nv.NVML_TEMPERATURE_GPU))
+        except Exception:
+            pass
+        try:
+            fv = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_MEMORY_TEMP])[0]
+            if fv.nvmlReturn == 0:
+                self.temps[f"mem_temp_c_{tag}"] = int(fv.value.uiVal)
+        except Exception:
+            pass
 
     def _run(self):
         nv = self.nv
@@ -85,6 +102,7 @@ class ClockSampler:
 
     def start(self):
         if self.ok:
+            self._thermals("start")
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
 
@@ -92,13 +110,14 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+            self._thermals("end")
 
     def report(self):
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": [], "samples": 0}
         names = [v for k, v in self.REASONS.items() if self.reasons & k]
         return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max,
-                "reasons": names, "samples": len(self.samples)}
+                "reasons": names, "samples": len(self.samples), **self.temps}
 
 
 def build_scene(world: int, rank: int, n: int):

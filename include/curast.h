@@ -67,7 +67,8 @@ enum curast_counter {
     CURAST_C_SLICE_SNAP = 26, /* 4 slots: fp64-queue size after each slice      */
     CURAST_C_PROVED = 30,     /* fp64-queue entries decided by the fp32 prover  */
     CURAST_C_CLAIM1B = 31,    /* second flat-table claim counter (die halves)   */
-    CURAST_COUNTER_SLOTS = 32
+    CURAST_C_QXHOLES = 32,    /* fp64-queue slots reserved but left empty       */
+    CURAST_COUNTER_SLOTS = 40
 };
 
 enum curast_error {
@@ -93,6 +94,8 @@ enum curast_error {
  * kernel's shared-memory slot j + j/16 (one pad slot per 16 keeps the
  * lookups of strip meshes bank-conflict free), and the u8 triangle record
  * holds that slot number */
+/* fp64-queue slots a stage-1 warp reserves at a time (holes: tag -1) */
+#define CURAST_QX_RES 128
 #define CURAST_MESHLET_TRIS 126
 #define CURAST_MESHLET_BYTES 384
 #define CURAST_MESHLET_MAX_VERTS 240

@@ -20,7 +20,9 @@ IDX_U32, IDX_PACKED = 0, 1
 C_Q2, C_Q3, C_S1, C_S2, C_S3 = 0, 1, 2, 10, 15
 C_CLAIM1, C_CLAIM2, C_CLAIM3, C_EXACT, C_QX = 16, 17, 18, 19, 20
 C_PROVED = 30
-COUNTER_SLOTS = 32
+QX_RES = 128       # CURAST_QX_RES: fp64-queue slots a stage-1 warp reserves at a time
+C_QXHOLES = 32     # fp64-queue slots reserved by a warp but left empty (tag -1)
+COUNTER_SLOTS = 40
 FILTER_FLOATS = 16
 INST_BLOCK = 16          # CURAST_INST_BLOCK: instances per instanced work unit
 QX_WORDS = 6

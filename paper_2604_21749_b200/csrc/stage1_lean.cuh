@@ -41,29 +41,44 @@ __device__ __forceinline__ unsigned lean_decide(float mnx, float mxx, float mny,
     return bits;
 }
 
-__device__ __forceinline__ unsigned lean_bits(const LeanConsts &F, const float *x, const float *y,
-                                              const float *z, float W, float H, float slack,
-                                              bool tiny) {
-    float2 P[3];
-    float D[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        D[k] = __fmaf_rn(F.dz, z[k], __fmaf_rn(F.dy, y[k], __fmaf_rn(F.dx, x[k], F.d3)));
-        float2 t = __ffma2_rn(F.cx, make_float2(x[k], x[k]), F.c3);
-        t = __ffma2_rn(F.cy, make_float2(y[k], y[k]), t);
-        t = __ffma2_rn(F.cz, make_float2(z[k], z[k]), t);
-        const float r = rcp_approx(D[k]);
-        P[k] = __fmul2_rn(t, make_float2(r, r));
-    }
-    const float dmin = fminf(D[0], fminf(D[1], D[2]));
-    const float mnx = fminf(P[0].x, fminf(P[1].x, P[2].x));
-    const float mxx = fmaxf(P[0].x, fmaxf(P[1].x, P[2].x));
-    const float mny = fminf(P[0].y, fminf(P[1].y, P[2].y));
-    const float mxy = fmaxf(P[0].y, fmaxf(P[1].y, P[2].y));
+// One projected vertex: P = (X', Y') / d', D = d' (the per-vertex half of
+// lean_bits; a strip vertex shared by several triangles is projected once).
+struct LeanV {
+    float2 P;
+    float D;
+};
+
+__device__ __forceinline__ LeanV lean_vertex(const LeanConsts &F, float x, float y, float z) {
+    LeanV v;
+    v.D = __fmaf_rn(F.dz, z, __fmaf_rn(F.dy, y, __fmaf_rn(F.dx, x, F.d3)));
+    float2 t = __ffma2_rn(F.cx, make_float2(x, x), F.c3);
+    t = __ffma2_rn(F.cy, make_float2(y, y), t);
+    t = __ffma2_rn(F.cz, make_float2(z, z), t);
+    const float r = rcp_approx(v.D);
+    v.P = __fmul2_rn(t, make_float2(r, r));
+    return v;
+}
+
+// The per-triangle half: symmetric in the three vertices (min / max only).
+__device__ __forceinline__ unsigned lean_bits_v(const LeanConsts &F, const LeanV &a,
+                                                const LeanV &b, const LeanV &c, float W, float H,
+                                                float slack, bool tiny) {
+    const float dmin = fminf(a.D, fminf(b.D, c.D));
+    const float mnx = fminf(a.P.x, fminf(b.P.x, c.P.x));
+    const float mxx = fmaxf(a.P.x, fmaxf(b.P.x, c.P.x));
+    const float mny = fminf(a.P.y, fminf(b.P.y, c.P.y));
+    const float mxy = fmaxf(a.P.y, fmaxf(b.P.y, c.P.y));
     const float M = fmaxf(fmaxf(fabsf(mnx), fabsf(mxx)), fmaxf(fabsf(mny), fabsf(mxy)));
     float eps = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(dmin);
     eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, slack));
     return lean_decide(mnx, mxx, mny, mxy, eps, dmin > F.near_hi, W, H, tiny);
+}
+
+__device__ __forceinline__ unsigned lean_bits(const LeanConsts &F, const float *x, const float *y,
+                                              const float *z, float W, float H, float slack,
+                                              bool tiny) {
+    return lean_bits_v(F, lean_vertex(F, x[0], y[0], z[0]), lean_vertex(F, x[1], y[1], z[1]),
+                       lean_vertex(F, x[2], y[2], z[2]), W, H, slack, tiny);
 }
 
 // Fast-path decision for a triangle of a chunk proven (chunk_class) to lie
@@ -340,10 +355,81 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean(const curast_frame_t f, i
 // lean_range-based k_s1_lean below carries the experiment switches and
 // costs 5% more instructions and some spills (measured r01: 418 M vs 398 M
 // warp instructions on config B).
-// PFI: L1 prefetch of the next step's index lines.  STRIP: the quad-strip
-// vertex-reuse gathers below.  Both measured box-dependent (config B stage 1
-// 0.77 ms on one B200, 1.10 ms on another, where the plain kernel is
-// 0.80-0.84 ms on both), so the default instantiation has neither.
+// Per-warp slot reservation in the fp64 queue.  One u64 atomicAdd per warp
+// step on the single queue counter serialises at the L2: ~1.5 G same-address
+// atomics/s measured on the B200 (tools/atomic_probe.cu: 0.52 ms for the 780 K
+// steps of a config-B frame, the filter's own length), and the filter ran at
+// that floor, bimodally slower in some processes.  A warp instead takes
+// CURAST_QX_RES slots at a time and hands them to its steps; a step that
+// overruns the block continues in the next one.  The warp's final rest is left
+// as holes (tag -1), skipped by the fp64 pass (which counts them in
+// CURAST_C_QXHOLES).  The queue counter therefore counts reserved slots, which
+// is what the host sizes the queue by.  Slots are 32-bit (< 2^32 entries).
+struct QxReserve {
+    unsigned next;   // next free reserved slot
+    int left;        // reserved slots left
+};
+
+// The slots of one step: step-relative index i < split goes to base + i, the
+// rest to base2 + i (the next block, base2 = block - split).
+struct QxSlots {
+    unsigned base, base2;
+    int split;
+    __device__ __forceinline__ long long at(int i) const {
+        return (long long)(i < split ? base + (unsigned)i : base2 + (unsigned)i);
+    }
+};
+
+// tot consecutive slots for this step (whole warp, 0 < tot <= 128)
+__device__ __forceinline__ QxSlots qx_reserve(QxReserve &R, unsigned long long *qcount, int tot,
+                                              int lane) {
+    QxSlots q;
+    unsigned base = 0, base2 = 0;
+    int split = 0;
+    if (lane == 0) {
+        const unsigned next = R.next;
+        const int left = R.left;
+        base = next;
+        if (left < tot) {
+            const unsigned blk = (unsigned)atomicAdd(qcount, (unsigned long long)CURAST_QX_RES);
+            split = left;
+            base2 = blk - (unsigned)left;
+            R.next = blk + (unsigned)(tot - left);
+            R.left = CURAST_QX_RES - (tot - left);
+        } else {
+            split = tot;
+            R.next = next + (unsigned)tot;
+            R.left = left - tot;
+        }
+    }
+    q.base = __shfl_sync(0xffffffffu, base, 0);
+    q.split = __shfl_sync(0xffffffffu, split, 0);
+    q.base2 = q.split < tot ? __shfl_sync(0xffffffffu, base2, 0) : 0u;   // uniform branch
+    return q;
+}
+
+// the warp's final rest becomes holes
+__device__ __forceinline__ void qx_reserve_close(const curast_frame_t &f, const QxReserve &R, int lane) {
+    __syncwarp();
+    const unsigned b = R.next;
+    const int n = R.left;
+#pragma unroll 1
+    for (int j = lane; j < n; j += 32)
+        if ((long long)b + j < f.qx_cap) f.qx[CURAST_QX_WORDS * ((long long)b + j) + CURAST_QX_TAG] = -1;
+}
+
+// adds the packed (frustum | tiny << 16) lane counts to the frame counters
+__device__ __forceinline__ void lean_flush16(const curast_frame_t &f, unsigned c) {
+    unsigned long long cnt[2] = {c & 0xffffu, c >> 16};
+    flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+    flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+}
+
+// PFI: L1 prefetch of the next step's index lines (switch only).  STRIP:
+// the quad-strip vertex-reuse gathers below (the default instantiation:
+// config B stage-1 filter 526 vs 544 us without).  Before the per-warp queue
+// reservation both were bimodal across processes (0.77 / 1.10 ms stage 1):
+// the same-address queue atomics were the floor, see qx_reserve.
 // DIE: two claim sequences, one per half of the SM ids (the two dies of a
 // B200): SMs of the lower half walk the chunks of the first half of the
 // table, the upper half the second, and a half that runs out continues in
@@ -357,12 +443,21 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
     constexpr int CHUNK = kS1Chunk, STEP = 32 * TPL;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned n_frustum = 0, n_tiny = 0;
+    // frustum / tiny counts as two 16-bit fields of one register (one
+    // register less than two counters: the loop runs at the 64-register cap);
+    // flushed before a field can pass 2^15 (<= 64 per lane per chunk)
+    unsigned cnt16 = 0;
     const float W = (float)f.width, H = (float)f.height;
     const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
     const bool tiny = f.tiny_cull != 0;
     const int64_t total = min(cend, __ldg(f.unit_chunk_prefix + f.n_units));
     unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+    // lane 0's reservation state lives in shared memory: the filter loop is
+    // at the 64-register cap (two more live registers spill)
+    __shared__ QxReserve sres[8];
+    QxReserve &R = sres[threadIdx.x >> 5];
+    if (lane == 0) R = QxReserve{0u, 0};
+    __syncwarp();
 
     for (;;) {
         long long c = 0, item = 0, lo = 0, hi = 0;
@@ -397,6 +492,10 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
         lo = __shfl_sync(0xffffffffu, lo, 0);
         hi = __shfl_sync(0xffffffffu, hi, 0);
 
+        if (__any_sync(0xffffffffu, cnt16 & 0x80008000u)) {
+            lean_flush16(f, cnt16);
+            cnt16 = 0;
+        }
         LeanConsts F;
         lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);
         const int64_t vo = __ldg(f.item_vtx_off + item);
@@ -473,16 +572,18 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
                 for (int k = 0; k < 3 * TPL; ++k) gather(k);
             }
             unsigned need = 0, fr = 0;
+            unsigned bt[TPL];
+#pragma unroll
+            for (int t = 0; t < TPL; ++t)
+                bt[t] = lean_bits(F, px + 3 * t, py + 3 * t, pz + 3 * t, W, H, slack, tiny);
 #pragma unroll
             for (int t = 0; t < TPL; ++t) {
-                const unsigned bits = lean_bits(F, px + 3 * t, py + 3 * t, pz + 3 * t, W, H, slack, tiny);
                 if (t < nv) {
-                    need |= (bits & 1u) << t;
-                    fr |= (bits >> 1) << t;
+                    need |= (bt[t] & 1u) << t;
+                    fr |= (bt[t] >> 1) << t;
                 }
             }
-            n_frustum += __popc(fr);
-            n_tiny += nv - __popc(need) - __popc(fr);
+            cnt16 += (unsigned)__popc(fr) + ((unsigned)(nv - __popc(need) - __popc(fr)) << 16);
             unsigned b[TPL];
             int tot = 0;
 #pragma unroll
@@ -491,13 +592,12 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
                 tot += __popc(b[t]);
             }
             if (tot) {
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(qcount, (unsigned long long)tot);
-                base = __shfl_sync(0xffffffffu, base, 0);
+                const QxSlots qs = qx_reserve(R, qcount, tot, lane);
+                int base = 0;
 #pragma unroll
                 for (int t = 0; t < TPL; ++t) {
                     if ((need >> t) & 1u) {
-                        const long long slot = (long long)base + __popc(b[t] & lt_mask);
+                        const long long slot = qs.at(base + __popc(b[t] & lt_mask));
                         if (slot < f.qx_cap) {
                             // positions travel with the entry: the fp64 kernel
                             // does not re-gather them from HBM
@@ -514,9 +614,8 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
             }
         }
     }
-    unsigned long long cnt[2] = {n_frustum, n_tiny};
-    flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
-    flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+    qx_reserve_close(f, R, lane);
+    lean_flush16(f, cnt16);
 }
 
 // Per-triangle lean kernel over the lane-major index steps (indices_ilv):

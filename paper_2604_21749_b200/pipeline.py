@@ -32,6 +32,9 @@ from .device import PackedUpload, filter_rows, scene_geometry, workspace
 from .scene import (CLEAR, CapacityError, DrawList, Framebuffer, build_draw_list,
                     projection_vector)
 
+# resident stage-1 warps (<= 160 SMs x 32) x one reservation block each
+QX_HOLE_SLACK = 160 * 32 * N.QX_RES
+
 INST_BLOCK = N.INST_BLOCK
 
 # CURAST_FILTER=0 disables the fp32 cull filter (every triangle fp64) — a
@@ -341,8 +344,12 @@ class PreparedFrame:
             per_unit = np.minimum(gc - k0, INST_BLOCK)
         else:
             per_unit = np.zeros(0, np.int64)
-        self.qx_need_max = int((self.unit_hi - self.unit_lo).sum()
-                               + ((self.iunit_hi - self.iunit_lo) * per_unit).sum())
+        # entries <= triangles; per-warp reservations (CURAST_QX_RES) add
+        # holes: < 1 step per block of >= 129 used slots, plus each warp's
+        # final rest
+        flat = int((self.unit_hi - self.unit_lo).sum())
+        self.qx_need_max = int(2 * flat + ((self.iunit_hi - self.iunit_lo) * per_unit).sum()
+                               + QX_HOLE_SLACK)
         self._size_queues(DEVICE_Q2_INITIAL, DEVICE_Q3_INITIAL)
 
     def _size_queues(self, want2: int, want3: int, wantx: int = 0):
@@ -418,7 +425,8 @@ class PreparedFrame:
             c = self.read_counters()
             nx = int(c[N.C_QX])
             if nx > self.qx_alloc:
-                self._size_queues(self.q2_alloc, self.q3_alloc, nx)
+                # reserved slots vary a little run to run: leave headroom
+                self._size_queues(self.q2_alloc, self.q3_alloc, nx + nx // 32 + QX_HOLE_SLACK // 4)
                 continue
             n2, n3 = int(c[N.C_Q2]), int(c[N.C_Q3])
             if n2 > self.s2_cap:
@@ -454,7 +462,8 @@ class PreparedFrame:
         st.stage3 = Stage3Stats(entries=int(c[N.C_Q3]), fragments=int(c[N.C_S3]))
         st.merge_s, st.stage1_s, st.stage2_s, st.stage3_s = secs
         st.proved_fp32 = int(c[N.C_PROVED])
-        st.exact_fallbacks = int(c[N.C_QX]) + int(c[N.C_EXACT]) - st.proved_fp32
+        st.exact_fallbacks = (int(c[N.C_QX]) - int(c[N.C_QXHOLES]) + int(c[N.C_EXACT])
+                              - st.proved_fp32)
         return st
 
 

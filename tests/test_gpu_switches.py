@@ -55,6 +55,8 @@ sys.exit(1 if bad else 0)
     {"CURAST_XMINB": "8"},
     {"CURAST_INSTANCED_KERNEL": "1"},
     {"CURAST_S1": "strip"},
+    {"CURAST_S1": "plain"},
+    {"CURAST_S1": "pfi"},
     {"CURAST_S1": "die"},
     {"CURAST_S1": "fused", "CURAST_XMINB": "4"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))

@@ -29,5 +29,7 @@ for e in prof.events():
         times.setdefault(e.name[:40], []).append(e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total)
 out = {k: round(sum(v) / len(v), 1) for k, v in times.items()}
 fb_ptr = pf.fb.data_ptr()
-print(json.dumps({"us": out, "fb": hex(fb_ptr), "pos": hex(pf.geo.positions.data_ptr()),
+c = pf.read_counters()
+from paper_2604_21749_b200 import _native as N  # noqa: E402
+print(json.dumps({"us": out, "qx_slots": int(c[N.C_QX]), "qx_holes": int(c[N.C_QXHOLES]), "fb": hex(fb_ptr), "pos": hex(pf.geo.positions.data_ptr()),
                   "idx": hex(pf.geo.indices.data_ptr())}))
