@@ -635,6 +635,10 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_ilv(const curast_frame_t 
     const bool tiny = f.tiny_cull != 0;
     const int64_t total = min(cend, __ldg(f.unit_chunk_prefix + f.n_units));
     unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+    __shared__ QxReserve sres[8];
+    QxReserve &R = sres[threadIdx.x >> 5];
+    if (lane == 0) R = QxReserve{0u, 0};
+    __syncwarp();
     for (;;) {
         long long c = 0, item = 0, lo = 0, hi = 0;
         if (lane == 0) {
@@ -698,19 +702,19 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_ilv(const curast_frame_t 
                 tot += __popc(b[t]);
             }
             if (tot) {
-                unsigned long long qb = 0;
-                if (lane == 0) qb = atomicAdd(qcount, (unsigned long long)tot);
-                qb = __shfl_sync(0xffffffffu, qb, 0);
+                const QxSlots qs = qx_reserve(R, qcount, tot, lane);
+                int qb = 0;
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     if ((need >> t) & 1u)
-                        qx_write(f, (long long)qb + __popc(b[t] & lt_mask), px + 3 * t, py + 3 * t,
+                        qx_write(f, qs.at(qb + __popc(b[t] & lt_mask)), px + 3 * t, py + 3 * t,
                                  pz + 3 * t, tag + tb + 32 * t);
                     qb += __popc(b[t]);
                 }
             }
         }
     }
+    qx_reserve_close(f, R, lane);
     unsigned long long cnt[2] = {n_frustum, n_tiny};
     flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
     flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
@@ -936,6 +940,10 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) 
     const bool tiny = f.tiny_cull != 0;
     const int64_t total = __ldg(f.inst_unit_chunk_prefix + f.n_inst_units);
     unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+    __shared__ QxReserve sres[8];
+    QxReserve &R = sres[threadIdx.x >> 5];
+    if (lane == 0) R = QxReserve{0u, 0};
+    __syncwarp();
 
     for (;;) {
         long long c = 0, g = 0, lo = 0, hi = 0;
@@ -984,11 +992,9 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) 
             if (valid && bits == 0u) ++n_tiny;
             const unsigned b = __ballot_sync(0xffffffffu, need);
             if (b) {
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(qcount, (unsigned long long)__popc(b));
-                base = __shfl_sync(0xffffffffu, base, 0);
+                const QxSlots qs = qx_reserve(R, qcount, __popc(b), lane);
                 if (need) {
-                    const long long slot = (long long)base + __popc(b & lt_mask);
+                    const long long slot = qs.at(__popc(b & lt_mask));
                     if (slot < f.qx_cap) {
                         int64_t *e = f.qx + CURAST_QX_WORDS * slot;
                         *(float4 *)e = make_float4(x[0], y[0], z[0], x[1]);
@@ -1001,6 +1007,7 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) 
         }
       }
     }
+    qx_reserve_close(f, R, lane);
     unsigned long long cnt[2] = {n_frustum, n_tiny};
     flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
     flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
