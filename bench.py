@@ -363,11 +363,19 @@ def run_reference(args):
     steps = args.steps
     warm = max(args.warmup, 1)
     budget = 150.0                      # whole run within a few minutes
-    probe = max(1, total // 100)
-    _, _, _, _, dt = oh.render_context(ctx, cc, workers=cores, batch=4096,
-                                       work_range=(0, probe), s2_cap=1 << 20, s3_cap=1 << 20)
-    rate = probe / max(dt, 1e-9)
-    sample = int(min(total, max(probe, rate * budget / (steps + warm))))
+    # the oracle call has a fixed cost (~0.4 s: per-worker frame buffers and
+    # their merge) besides its per-triangle work: two probes separate them, and
+    # a step is never smaller than a quarter of the frame, so the fixed cost
+    # does not dominate the reported rate when K is large
+    dts = []
+    probes = (max(1, total // 50), max(2, total // 10))
+    for n in probes:
+        dts.append(oh.render_context(ctx, cc, workers=cores, batch=4096, work_range=(0, n),
+                                     s2_cap=1 << 20, s3_cap=1 << 20)[4])
+    rate = (probes[1] - probes[0]) / max(dts[1] - dts[0], 1e-9)
+    fixed = max(0.0, dts[0] - probes[0] / rate)
+    per_step = budget / (steps + warm)
+    sample = int(min(total, max(total // 4, rate * max(per_step - fixed, 0.0))))
     times = []
     for k in range(steps + warm):
         b = (k * sample) % max(1, total - sample + 1)
