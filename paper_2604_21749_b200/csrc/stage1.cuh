@@ -6,6 +6,7 @@
 #pragma once
 #include "exact.cuh"
 #include "filter.cuh"
+#include "qxres.cuh"
 
 namespace curast {
 
@@ -170,6 +171,11 @@ __device__ __forceinline__ int filter_fast2(const FilterPairs &F, const float *v
 template <int PF, int IF, int MINB, bool PAIR, bool WP = false>
 __global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_t f) {
     const int lane = threadIdx.x & 31;
+    unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+    __shared__ QxReserve sres[W_THREADS / 32];
+    QxReserve &R = sres[threadIdx.x >> 5];
+    if (lane == 0) R = QxReserve{0u, 0};
+    __syncwarp();
     unsigned int n_frustum = 0, n_tiny = 0;
     const float W = (float)f.width, H = (float)f.height;
     const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
@@ -242,15 +248,12 @@ __global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_
             }
             const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
             if (wtotal) {
-                unsigned long long base = 0;
-                if (lane == 31)
-                    base = atomicAdd((unsigned long long *)(f.counters + CURAST_C_QX),
-                                     (unsigned long long)wtotal);
-                base = __shfl_sync(0xffffffffu, base, 31);
-                int64_t slot = (int64_t)base + incl - mine;
+                const QxSlots qs = qx_reserve(R, qcount, wtotal, lane);
+                int si = incl - mine;
                 while (need) {
                     const int t = __ffs(need) - 1;
                     need &= need - 1;
+                    const long long slot = qs.at(si);
                     if (slot < f.qx_cap) {
                         int64_t *e = f.qx + CURAST_QX_WORDS * slot;
                         if (WP && PF == CURAST_POS_U16) {
@@ -272,11 +275,12 @@ __global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_
                         }
                         e[CURAST_QX_TAG] = tag + o + t;
                     }
-                    ++slot;
+                    ++si;
                 }
             }
         }
     }
+    qx_reserve_close(f, R, lane);
     unsigned long long cnt[2] = {n_frustum, n_tiny};
     flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
     flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
