@@ -113,12 +113,6 @@ __device__ __forceinline__ unsigned lean_fast_bits(const LeanConsts &F, const fl
     return (ext && (tx || ty)) ? 0u : 1u;
 }
 
-// words 4-5 of a queue entry (z of the third vertex, zero-padded, and the
-// tag) as one 16-byte store
-__device__ __forceinline__ void qx_tail(int64_t *e, float z2, long long tag) {
-    *(longlong2 *)(e + 4) = make_longlong2((long long)__float_as_uint(z2), tag);
-}
-
 // fp64 queue entry: the 9 object-space positions + tag (CURAST_QX_WORDS)
 __device__ __forceinline__ void qx_write(const curast_frame_t &f, long long slot, const float *x,
                                          const float *y, const float *z, long long tag) {
@@ -126,7 +120,8 @@ __device__ __forceinline__ void qx_write(const curast_frame_t &f, long long slot
     int64_t *e = f.qx + CURAST_QX_WORDS * slot;
     *(float4 *)e = make_float4(x[0], y[0], z[0], x[1]);
     *(float4 *)(e + 2) = make_float4(y[1], z[1], x[2], y[2]);
-    qx_tail(e, z[2], tag);
+    *(float2 *)(e + 4) = make_float2(z[2], 0.0f);
+    e[CURAST_QX_TAG] = tag;
 }
 
 struct LeanCtx {
@@ -548,7 +543,8 @@ __global__ void __launch_bounds__(256, MINB) k_s1_lean_flat(const curast_frame_t
                             *(float4 *)e = make_float4(px[3 * t], py[3 * t], pz[3 * t], px[3 * t + 1]);
                             *(float4 *)(e + 2) = make_float4(py[3 * t + 1], pz[3 * t + 1],
                                                              px[3 * t + 2], py[3 * t + 2]);
-                            qx_tail(e, pz[3 * t + 2], tag + o + t);
+                            *(float2 *)(e + 4) = make_float2(pz[3 * t + 2], 0.0f);
+                            e[CURAST_QX_TAG] = tag + o + t;
                         }
                     }
                     base += __popc(b[t]);
@@ -941,7 +937,8 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_lean(const curast_frame_t f) 
                         int64_t *e = f.qx + CURAST_QX_WORDS * slot;
                         *(float4 *)e = make_float4(x[0], y[0], z[0], x[1]);
                         *(float4 *)(e + 2) = make_float4(y[1], z[1], x[2], y[2]);
-                        qx_tail(e, z[2], (item << 40) | local);
+                        *(float2 *)(e + 4) = make_float2(z[2], 0.0f);
+                        e[CURAST_QX_TAG] = (item << 40) | local;
                     }
                 }
             }
