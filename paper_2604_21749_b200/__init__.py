@@ -15,6 +15,7 @@ from .scene import (CLEAR, MAX_TRIANGLE_ID, TRIANGLE_ID_MASK, Camera, CapacityEr
 from .pipeline import (PreparedFrame, build_context, classify_route,
                        clip_triangle_near_plane, render_draw_list, render_frame)
 from .meshio import ParseError, load_mesh, save_mesh
+from .resolve import debug_view, downsample, resolve_frame
 
 __version__ = "0.1.0"
 
@@ -23,6 +24,6 @@ __all__ = [
     "FrameStats", "MAX_TRIANGLE_ID", "Mesh", "ParseError", "PreparedFrame", "RasterConfig",
     "SceneNode", "ShadingConfig", "Stage1Stats", "Stage2Stats", "Stage3Stats",
     "TRIANGLE_ID_MASK", "build_context", "build_draw_list", "classify_route",
-    "clip_triangle_near_plane", "load_mesh", "pack_fragment", "projection_vector",
-    "render_draw_list", "render_frame", "save_mesh", "unpack_fragment",
+    "clip_triangle_near_plane", "debug_view", "downsample", "load_mesh", "pack_fragment", "projection_vector",
+    "render_draw_list", "render_frame", "resolve_frame", "save_mesh", "unpack_fragment",
 ]

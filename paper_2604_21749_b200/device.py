@@ -68,6 +68,19 @@ class DeviceMesh:
         idx = mesh.indices
         self.triangle_count = int(mesh.triangle_count)
         self.device = device
+        if hasattr(mesh, "generate"):
+            # generated in HBM (generators.DeviceGeneratedMesh, config E):
+            # float32-exact by construction, no host copy
+            p4, i32 = mesh.generate(device)
+            self.pos_format = N.POS_F32
+            self.positions = p4
+            self.vertex_count = int(p4.shape[0])
+            self.qgrid = np.zeros(6)
+            self.pos_bound = p4[:, :3].abs().amax(dim=0).double().cpu().numpy()
+            self.idx_format = N.IDX_U32
+            self.indices = i32
+            self.pack = (0, 32)
+            return
         if is_quantized_positions(pos):
             self.pos_format = N.POS_U16
             # u16[V][4] (x, y, z, 0): one 64-bit load per vertex in-kernel

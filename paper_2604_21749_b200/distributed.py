@@ -80,18 +80,33 @@ def _ncheck(rc, what):
         raise N.NativeError(f"{what}: {nccl_lib().curast_nccl_last_error().decode()}")
 
 
+def _group_key(group):
+    """Cache key of a process group (None = the default group)."""
+    return "default" if group is None else id(group)
+
+
+def _group_src(group) -> int:
+    """Global rank of the group's rank 0 (broadcast sources are global ranks)."""
+    if group is None:
+        return 0
+    return dist.get_global_rank(group, 0)
+
+
 class NcclComm:
-    """A raw NCCL communicator over the ranks of the default process group."""
+    """A raw NCCL communicator over the ranks of ``group`` (default: the
+    default process group).  The ncclUniqueId is broadcast from the group's
+    first rank; ``close()`` destroys the communicator."""
 
     def __init__(self, group=None):
         L = nccl_lib()
+        self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         buf = ctypes.create_string_buffer(128)
         if self.rank == 0:
             _ncheck(L.curast_nccl_unique_id(buf), "ncclGetUniqueId")
         obj = [bytes(buf.raw)]
-        dist.broadcast_object_list(obj, src=0, group=group)
+        dist.broadcast_object_list(obj, src=_group_src(group), group=group)
         self.comm = ctypes.c_void_p()
         _ncheck(L.curast_nccl_init(ctypes.byref(self.comm), obj[0], self.world, self.rank),
                 "ncclCommInitRank")
@@ -117,15 +132,58 @@ class NcclComm:
             self.comm = None
 
 
-class Compositor:
-    """Per-frame composite of a rank's visibility buffer (int64 CUDA tensor)."""
+_comms: dict = {}
 
-    def __init__(self, words: torch.Tensor, world: int):
+
+def group_comm(group=None) -> NcclComm:
+    """The cached NCCL communicator of ``group`` (created on first use, one
+    per group for the life of the process; ``close_comms()`` releases them).
+    A communicator per frame would leak one ncclComm and its buffers per
+    call."""
+    key = _group_key(group)
+    c = _comms.get(key)
+    if c is None or c.comm is None:
+        c = NcclComm(group)
+        _comms[key] = c
+    return c
+
+
+def close_comms() -> None:
+    """Destroy every cached communicator (call before destroy_process_group)."""
+    for c in _comms.values():
+        c.close()
+    _comms.clear()
+
+
+def _use_nccl(words: torch.Tensor, group) -> bool:
+    return (words.is_cuda and dist.get_backend(group) == "nccl"
+            and os.path.exists(NCCL_LIB))
+
+
+def _min_on_host(words: torch.Tensor, group) -> None:
+    """Unsigned-min all-reduce through a CPU process group (gloo): CUDA
+    words are staged through host memory."""
+    if words.is_cuda:
+        host = words.cpu()
+        composite_min_u64_(host, group)
+        words.copy_(host)
+    else:
+        composite_min_u64_(words, group)
+
+
+class Compositor:
+    """Per-frame composite of a rank's visibility buffer (int64 tensor) over
+    the ranks of ``group``: NCCL (ncclUint64 / ncclMin, cached communicator)
+    for CUDA words on an NCCL group, else the sign-flipped MIN all-reduce of
+    the group's backend (gloo, through host memory)."""
+
+    def __init__(self, words: torch.Tensor, world: int | None = None, group=None):
         self.words = words
-        self.world = world
+        self.group = group
+        self.world = dist.get_world_size(group) if world is None else int(world)
         self.launches_per_call = 1
-        if words.is_cuda and dist.get_backend() == "nccl" and os.path.exists(NCCL_LIB):
-            self.comm = NcclComm()
+        if _use_nccl(words, group):
+            self.comm = group_comm(group)
         else:
             self.comm = None
             self.launches_per_call = 3
@@ -134,12 +192,14 @@ class Compositor:
         if self.comm is not None:
             self.comm.allreduce_min(self.words)
         else:
-            composite_min_u64_(self.words)
+            _min_on_host(self.words, self.group)
 
-    def reduce_scatter_min(self, rank: int):
+    def reduce_scatter_min(self, rank: int | None = None):
         """Composite into stripes: this rank receives the unsigned-min of all
         ranks' words over its 1/world slice (self.stripe); the full VB exists
         once, distributed — the input of the striped resolve."""
+        if rank is None:
+            rank = dist.get_rank(self.group)
         n = self.words.numel()
         per = -(-n // self.world)
         if not hasattr(self, "stripe"):
@@ -153,15 +213,17 @@ class Compositor:
             self.comm.reduce_scatter_min(self._padded, self.stripe)
         else:
             full = self._padded.clone()
-            composite_min_u64_(full)
+            _min_on_host(full, self.group)
             self.stripe.copy_(full[rank * per:(rank + 1) * per])
         return self.stripe
 
 
 def render_sharded(draw_list, camera, cfg=None, *, group=None):
     """Sort-last frame on the calling rank's GPU: rasterize this rank's
-    global-ID shard, composite over all ranks; every rank returns the full
-    composite Framebuffer and its shard's FrameStats (sum them for totals)."""
+    global-ID shard, composite over all ranks of ``group``; every rank
+    returns the full composite Framebuffer and its shard's FrameStats (sum
+    them for totals).  Only the meshes of this rank's shard are uploaded
+    (``PreparedFrame(work_range=...)``)."""
     from .config import RasterConfig
     from .pipeline import PreparedFrame, build_context
     from .scene import Framebuffer
@@ -177,8 +239,7 @@ def render_sharded(draw_list, camera, cfg=None, *, group=None):
     c, secs = pf.run()
     st = pf.stats(c, secs)
     if world > 1:
-        comp = Compositor(pf.fb, world)
-        comp.allreduce_min()
+        Compositor(pf.fb, world, group).allreduce_min()
     return Framebuffer(camera.internal_width, camera.internal_height, device_words=pf.fb), st
 
 
@@ -220,23 +281,26 @@ def render_sharded_resolved(draw_list, camera, cfg=None, shading=None, *, root=0
     if per * world * W > words.numel():                    # pad with CLEAR rows
         words = torch.cat([words, words.new_full((per * world * W - words.numel(),), -1)])
     stripe = torch.empty(per * W, dtype=torch.int64, device=words.device)
-    if world > 1 and words.is_cuda and dist.get_backend(group) == "nccl" and os.path.exists(NCCL_LIB):
-        comm = NcclComm(group)
-        comm.reduce_scatter_min(words, stripe)
-        comm.close()
+    if world > 1 and _use_nccl(words, group):
+        group_comm(group).reduce_scatter_min(words, stripe)
     else:
         full = words.clone()
         if world > 1:
-            composite_min_u64_(full, group)
+            _min_on_host(full, group)
         stripe.copy_(full[rank * per * W:(rank + 1) * per * W])
     fb = Framebuffer(W, H, device_words=pf.fb)
     img, rst = resolve_frame_device(fb, draw_list, camera, shading, rows=(r0, n),
                                     stripe_words=stripe[:n * W])
     part = torch.zeros((per, W, 4), dtype=torch.uint8, device=img.device)
     part[:n] = img
-    if world > 1:
+    if world > 1 and _use_nccl(part, group):
         parts = [torch.empty_like(part) for _ in range(world)]
         dist.all_gather(parts, part, group=group)
+    elif world > 1:
+        hp = part.cpu()
+        hparts = [torch.empty_like(hp) for _ in range(world)]
+        dist.all_gather(hparts, hp, group=group)
+        parts = [p.to(part.device) for p in hparts]
     else:
         parts = [part]
     image = torch.cat(parts)[:H] if rank == root else None

@@ -175,3 +175,105 @@ def config_d(f32: bool = True, tris_per_mesh: int = 1_000_000, width: int = 3840
     scene = make_lantern_grid(40, 25, tris_per_mesh=tris_per_mesh, spacing=2.0, f32=f32)
     cam = Camera.look_at((0.0, 32.0, 45.0), (0.0, 0.0, 0.0), width=width, height=height)
     return scene, cam
+
+
+# --------------------------------------------------------------------- config E
+# Zorah-scale synthetic scene: distinct displaced grids
+# of n x n cells, tiled edge to edge into one terrain-like surface and seen
+# from above.  Each mesh's heights come from an integer hash of (column, row,
+# seed), so every coordinate is exactly representable in float32 and the host
+# (numpy) and device (torch) generators produce the same bits.
+E_DISPLACEMENT = 2.0 ** -20          # height step: |z| <= 512 steps ~ 4.9e-4
+
+
+def _e_heights(i, j, seed, xp):
+    """z of grid vertex (column i, row j) of mesh ``seed`` (int64 arrays of
+    numpy or torch): a 32-bit integer hash, 10 bits of it, centred."""
+    h = (i * 73856093) ^ (j * 19349663) ^ (seed * 83492791 + 0x9E3779B9)
+    h = h & 0xFFFFFFFF
+    h = (h ^ (h >> 15)) * 0x2C1B3C6D & 0xFFFFFFFF
+    h = (h ^ (h >> 12)) * 0x297A2D39 & 0xFFFFFFFF
+    h = h ^ (h >> 15)
+    v = ((h >> 8) & 0x3FF) - 512
+    return v
+
+
+def _e_axis(n: int) -> np.ndarray:
+    """Vertex coordinates along one axis, float32-rounded (the make_tessellated_quad axis)."""
+    return np.linspace(-0.5, 0.5, n + 1).astype(np.float32)
+
+
+E_AABB_Z = (-512 * E_DISPLACEMENT, 511 * E_DISPLACEMENT)
+
+
+def displaced_grid(n: int, seed: int) -> Mesh:
+    """Host-generated mesh ``seed`` of config E (float32-exact float64
+    positions, grid_indices topology)."""
+    ax = _e_axis(n).astype(np.float64)
+    j, i = np.meshgrid(np.arange(n + 1, dtype=np.int64), np.arange(n + 1, dtype=np.int64),
+                       indexing="ij")
+    z = _e_heights(i.ravel(), j.ravel(), np.int64(seed), np) * E_DISPLACEMENT
+    pos = np.stack([ax[i.ravel()], ax[j.ravel()], z.astype(np.float64)], axis=1)
+    aabb = np.array([[-0.5, -0.5, E_AABB_Z[0]], [0.5, 0.5, E_AABB_Z[1]]])
+    return Mesh(positions=pos, indices=grid_indices(n), triangle_count=2 * n * n, aabb=aabb,
+                name=f"egrid{seed}")
+
+
+class DeviceGeneratedMesh(Mesh):
+    """A config-E mesh whose geometry is generated on the GPU when it is
+    first made resident (device.device_mesh): no host copy of the positions
+    or indices ever exists, so a rank materialises only its shard's meshes
+    (SURVEY §7.3 hard part 5).  The bits equal ``displaced_grid(n, seed)``."""
+
+    def __init__(self, n: int, seed: int):
+        super().__init__(positions=("egrid", n, seed), indices=("egrid", n, seed),
+                         triangle_count=2 * n * n,
+                         aabb=np.array([[-0.5, -0.5, E_AABB_Z[0]], [0.5, 0.5, E_AABB_Z[1]]]),
+                         name=f"egrid{seed}")
+        self.grid_n = n
+        self.seed = seed
+
+    def vertex_count(self) -> int:
+        return (self.grid_n + 1) ** 2
+
+    def generate(self, device):
+        """(positions float32[V, 4] CUDA, indices int32[3T] CUDA)."""
+        import torch
+        n = self.grid_n
+        ax = torch.from_numpy(_e_axis(n)).to(device)
+        k = torch.arange((n + 1) ** 2, device=device, dtype=torch.int64)
+        i, j = k % (n + 1), k // (n + 1)
+        z = _e_heights(i, j, int(self.seed), torch).to(torch.float32) * E_DISPLACEMENT
+        pos = torch.zeros(((n + 1) ** 2, 4), dtype=torch.float32, device=device)
+        pos[:, 0] = ax[i]
+        pos[:, 1] = ax[j]
+        pos[:, 2] = z
+        c = torch.arange(n * n, device=device, dtype=torch.int64)
+        a = (c // n) * (n + 1) + c % n
+        b, cc = a + 1, a + n + 1
+        d = cc + 1
+        tri = torch.stack([a, cc, b, b, cc, d], dim=1).reshape(-1).to(torch.int32)
+        return pos, tri
+
+
+def config_e(n_meshes: int = 4750, n: int = 1414, seed: int = 0, width: int = 3840,
+             height: int = 2160, on_device: bool = False):
+    """E: ~19B unique triangles (4,750 distinct displaced n=1414 grids of
+    3,998,792 triangles = 18.99B), tiled edge to edge, overview camera
+    @3840x2160.  ``on_device`` makes each mesh a
+    DeviceGeneratedMesh (generated in HBM when a rank first needs it);
+    otherwise the meshes are host arrays (small instances, oracle-checkable)."""
+    cols = max(1, int(math.ceil(math.sqrt(n_meshes * width / height))))
+    rows = -(-n_meshes // cols)
+    scene = []
+    for k in range(n_meshes):
+        c, r = k % cols, k // cols
+        T = np.eye(4)
+        T[0, 3] = c - (cols - 1) / 2.0
+        T[1, 3] = r - (rows - 1) / 2.0
+        mesh = DeviceGeneratedMesh(n, seed + k) if on_device else displaced_grid(n, seed + k)
+        scene.append(SceneNode(mesh=mesh, transforms=[T]))
+    half = max(rows / 2.0, cols / 2.0 * height / width) * 1.02
+    dist = half / math.tan(math.radians(30.0))
+    cam = Camera.look_at((0.0, 0.0, dist), (0.0, 0.0, 0.0), width=width, height=height)
+    return scene, cam

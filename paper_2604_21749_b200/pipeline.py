@@ -109,6 +109,72 @@ def build_context(draw_list: DrawList, camera) -> RenderContext:
         max_instances=max_inst)
 
 
+def adopt_context(ctx, draw_list: DrawList, camera) -> RenderContext:
+    """Accept the reference's ``trirast.pipeline.RenderContext``
+    (pipeline.py:68-84: flattened f64 ``positions`` / u32 ``indices`` with
+    per-item ``item_vtx_off`` / ``item_idx_off``, ``prefix``, ``item_mv`` /
+    ``item_mw``) as the ``ctx`` of ``render_draw_list``: its concatenated
+    geometry becomes one device mesh addressed through the item offsets, and
+    its matrices and prefix are used as given.  The instancing groups are
+    rebuilt from the draw list (the reference builds them the same way,
+    pipeline.py:114-135).  The flat mesh is cached on the context object."""
+    if isinstance(ctx, RenderContext):
+        return ctx
+    for name in ("positions", "indices", "item_vtx_off", "item_idx_off", "item_mv", "prefix"):
+        if not hasattr(ctx, name):
+            raise TypeError(f"ctx has no '{name}': not a RenderContext of this package "
+                            "or of the reference (trirast.pipeline.RenderContext)")
+    own = build_context(draw_list, camera)
+    cached = getattr(ctx, "_curast_flat_mesh", None)
+    if cached is not None and cached[0] is ctx.positions and cached[1] is ctx.indices:
+        flat = cached[2]
+    else:
+        from .scene import Mesh
+        pos = np.ascontiguousarray(ctx.positions, dtype=np.float64).reshape(-1, 3)
+        idx = np.ascontiguousarray(ctx.indices, dtype=np.uint32).ravel()
+        aabb = (np.stack([pos.min(axis=0), pos.max(axis=0)]) if len(pos)
+                else np.zeros((2, 3)))
+        flat = Mesh(positions=pos, indices=idx, triangle_count=len(idx) // 3, aabb=aabb,
+                    name="reference_context")
+        try:
+            object.__setattr__(ctx, "_curast_flat_mesh", (ctx.positions, ctx.indices, flat))
+        except (AttributeError, TypeError):
+            pass
+    n = len(draw_list.items)
+    own.meshes = [flat]
+    own.item_mesh = np.zeros(n, dtype=np.int64)
+    own.item_vtx_off = np.asarray(ctx.item_vtx_off, dtype=np.int64).reshape(n)
+    own.item_idx_off = np.asarray(ctx.item_idx_off, dtype=np.int64).reshape(n)
+    own.item_mv = np.ascontiguousarray(ctx.item_mv, dtype=np.float64).reshape(n, 3, 4)
+    mw = getattr(ctx, "item_mw", None)
+    if mw is not None:
+        own.item_mw = np.ascontiguousarray(mw, dtype=np.float64).reshape(n, 3, 4)
+    own.prefix = np.asarray(ctx.prefix, dtype=np.int64)
+    return own
+
+
+def shard_items(ctx: RenderContext, work_range, inst_kernel: bool) -> np.ndarray:
+    """Boolean mask of the draw items a work range touches: the items whose
+    global-ID range intersects it (flat work space), or every item of the
+    instancing groups whose unique-triangle range intersects it (instanced
+    work space, pipeline.py:244).  A sort-last rank uploads only these items'
+    meshes (each GPU holds only its shard's geometry)."""
+    lo, hi = int(work_range[0]), int(work_range[1])
+    n = len(ctx.item_mesh)
+    if not inst_kernel:
+        s = ctx.prefix[:-1]
+        e = ctx.prefix[1:]
+        return (e > lo) & (s < hi) & (e > s)
+    gs = ctx.group_prefix[:-1]
+    ge = ctx.group_prefix[1:]
+    gsel = (ge > lo) & (gs < hi) & (ge > gs)
+    mask = np.zeros(n, dtype=bool)
+    for g in np.nonzero(gsel)[0]:
+        o = int(ctx.group_item_off[g])
+        mask[ctx.group_items[o:o + int(ctx.group_item_count[g])]] = True
+    return mask
+
+
 def _work_table(starts: np.ndarray, counts: np.ndarray, unit_ids: np.ndarray,
                 begin: int, end: int, chunk: int):
     """Units (items or groups) intersected with [begin, end) of their global
@@ -159,19 +225,32 @@ class PreparedFrame:
         self.device = device
         self.cfg = cfg
         self.camera = camera
+        self.draw_list = draw_list
         self.width = camera.internal_width
         self.height = camera.internal_height
         self.total = int(draw_list.total_triangles)
         self.n_items = len(draw_list.items)
         if ctx is None:
             ctx = build_context(draw_list, camera)
+        ctx = adopt_context(ctx, draw_list, camera)
         self.ctx = ctx
         self.instanced = (cfg.instancing == "on"
                           or (cfg.instancing == "auto" and ctx.max_instances >= 2))
         if use_filter is None:
             use_filter = _FILTER_DEFAULT
         self.use_filter = bool(use_filter) and cfg.force_stage < 2
-        self.geo = scene_geometry(ctx.meshes, device)
+        n = self.n_items
+        # geometry: every mesh of the draw list for a full frame; only the
+        # meshes of the items the work range touches for a shard
+        if work_range is None:
+            need = np.ones(n, dtype=bool)
+        else:
+            inst_space = self.instanced
+            need = shard_items(ctx, work_range, inst_space)
+        used = np.unique(ctx.item_mesh[need]) if n else np.zeros(0, np.int64)
+        self.mesh_ids = used
+        slot = {int(m): k for k, m in enumerate(used)}
+        self.geo = scene_geometry([ctx.meshes[int(m)] for m in used], device)
         geo = self.geo
         self.s2_cap = cfg.resolved_stage2_capacity(self.total)
         self.s3_cap = cfg.resolved_stage3_capacity(self.total)
@@ -179,24 +258,24 @@ class PreparedFrame:
         self.ws = ws
         self.fb = ws.framebuffer(self.width * self.height, fresh_fb)
 
-        n = self.n_items
-        vtx_off = np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64)
-        idx_off = np.asarray([geo.idx_off[i] for i in ctx.item_mesh], dtype=np.int64)
-        ml_off = np.asarray([geo.ml_off[i] for i in ctx.item_mesh], dtype=np.int64)
-        cb_off = np.asarray([geo.cb_off[i] for i in ctx.item_mesh], dtype=np.int64)
+        gslot = [slot.get(int(m), -1) if need[k] else -1 for k, m in enumerate(ctx.item_mesh)]
+        vtx_off = np.asarray([geo.vtx_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
+        vtx_off += ctx.item_vtx_off
+        idx_off = np.asarray([geo.idx_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
+        idx_off += ctx.item_idx_off
+        ml_off = np.asarray([geo.ml_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
+        cb_off = np.asarray([geo.cb_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
         p = projection_vector(camera)
         p0, p1 = float(p[0]), float(p[1])
         self.p0, self.p1 = p0, p1
-        pos_bound = np.stack([geo.meshes[i].pos_bound for i in ctx.item_mesh]) if n else \
-            np.zeros((0, 3))
-        qgrid = np.stack([geo.meshes[i].qgrid for i in ctx.item_mesh]) if n else np.zeros((0, 6))
-        pack = np.asarray([geo.meshes[i].pack for i in ctx.item_mesh], dtype=np.int64).reshape(n, 2)
+        pos_bound = (np.stack([geo.meshes[g].pos_bound if g >= 0 else np.zeros(3)
+                               for g in gslot]) if n else np.zeros((0, 3)))
+        qgrid = (np.stack([geo.meshes[g].qgrid if g >= 0 else np.zeros(6) for g in gslot])
+                 if n else np.zeros((0, 6)))
+        pack = np.asarray([geo.meshes[g].pack if g >= 0 else (0, 32) for g in gslot],
+                          dtype=np.int64).reshape(n, 2)
         filt = filter_rows(ctx.item_mv.reshape(n, 12), pos_bound, p0, p1, self.width,
                            self.height, float(camera.near), geo.pos_format)
-        if geo.pos_format == N.POS_U16:
-            # the fp32 filter decodes with these rounded grid values; make the
-            # bound cover them: |gmin| + |gsize| already sized in pos_bound
-            pass
 
         # Stage-1 kernel for instanced frames: the instanced one (a unique
         # triangle fetched once, tested under every instance) or the flat one
@@ -246,7 +325,7 @@ class PreparedFrame:
                    and os.environ.get("CURAST_ILV", "auto") != "0") \
             or os.environ.get("CURAST_ILV") == "1"
         ilv = geo.index_steps() if use_ilv else None
-        ilv_off = np.asarray([geo.ilv_off[i] for i in ctx.item_mesh], dtype=np.int64)
+        ilv_off = np.asarray([geo.ilv_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
         up = PackedUpload()
         k_prefix = up.add(ctx.prefix)
         k_mv = up.add(ctx.item_mv.reshape(-1))
@@ -357,13 +436,21 @@ class PreparedFrame:
         ax = min(max(1, self.qx_need_max), max(wantx, min(DEVICE_QX_INITIAL, self.qx_need_max),
                                                 ws.qx_alloc))
         ws.ensure_qx(ax)
+        ws.ensure_q2(min(self.s2_cap, max(want2, ws.q2_alloc)))
+        ws.ensure_q3(min(self.s3_cap, max(want3, ws.q3_alloc)))
+        self._bind_queues()
+
+    def _bind_queues(self):
+        """Point the frame at the workspace's current queues.  The queues are
+        shared per device and grow-only: another frame may have replaced them
+        since this one was sized, so ``launch`` re-binds, and the frame keeps
+        references to the tensors its pointers (and any captured graph) use
+        so that memory is never handed back to the allocator under them."""
+        ws = self.ws
+        self._queues = (ws.qx, ws.q2, ws.q3)
         self.qx_alloc = ws.qx_alloc
         self.frame.qx = ws.qx.data_ptr()
         self.frame.qx_cap = self.qx_alloc
-        a2 = min(self.s2_cap, max(want2, ws.q2_alloc))
-        a3 = min(self.s3_cap, max(want3, ws.q3_alloc))
-        ws.ensure_q2(a2)
-        ws.ensure_q3(a3)
         self.q2_alloc = max(0, min(self.s2_cap, ws.q2_alloc))
         self.q3_alloc = max(0, min(self.s3_cap, ws.q3_alloc))
         self.frame.q2 = ws.q2.data_ptr()
@@ -371,10 +458,33 @@ class PreparedFrame:
         self.frame.q3 = ws.q3.data_ptr()
         self.frame.q3_cap = self.q3_alloc
 
+    def _queues_current(self) -> bool:
+        ws = self.ws
+        q = self._queues
+        return q[0] is ws.qx and q[1] is ws.q2 and q[2] is ws.q3
+
+    def refresh(self, new_framebuffer: bool = True):
+        """Reuse this prepared frame for another call with the same inputs:
+        re-upload the per-frame descriptors (one pinned H2D copy, as every
+        frame does) and, for a caller that keeps the previous frame's words,
+        bind a new visibility buffer.  The host-side setup (filter rows,
+        work table, packing) is not redone."""
+        up = self.upload
+        up.dev.copy_(up.host, non_blocking=True)
+        if new_framebuffer:
+            self.fb = self.ws.framebuffer(self.width * self.height, True)
+            self.frame.fb = self.fb.data_ptr()
+
     def launch(self, stream=None, events=None):
         """Enqueue clear + stages 1-3 on ``stream`` (default: torch's current)."""
         L = N.lib()
         st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        if not self._queues_current():
+            ws = self.ws
+            if ws.qx is None or ws.q2 is None or ws.q3 is None:
+                self._size_queues(self.q2_alloc, self.q3_alloc, self.qx_alloc)
+            else:
+                self._bind_queues()
         fp = ctypes.byref(self.frame)
         if events:
             events[0].record()
@@ -397,8 +507,8 @@ class PreparedFrame:
         instead of five kernel launches through ctypes.  Run the frame once
         first (``run()``) so the device queues are sized; replay with
         ``graph.replay()`` and read the counters as after ``launch``.  The
-        graph keeps this frame's device pointers: re-capture after
-        ``_size_queues`` grows a queue."""
+        graph keeps this frame's device pointers (the frame keeps those
+        buffers alive): re-capture after a queue grew (``stale_graph``)."""
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
@@ -408,7 +518,14 @@ class PreparedFrame:
         torch.cuda.synchronize(self.device)
         with torch.cuda.graph(g):
             self.launch()
+        self._graph_queues = self._queues
         return g
+
+    @property
+    def stale_graph(self) -> bool:
+        """True when the queues moved since ``capture()`` (the graph still
+        writes into this frame's previous, still-referenced buffers)."""
+        return getattr(self, "_graph_queues", None) is not self._queues
 
     def read_counters(self) -> np.ndarray:
         ws = self.ws
@@ -467,21 +584,69 @@ class PreparedFrame:
         return st
 
 
+_FRAME_CACHE_MAX = 4
+_frame_cache: dict = {}
+
+
+def _camera_key(camera):
+    return (np.asarray(camera.position, dtype=np.float64).tobytes(),
+            np.asarray(camera.view_transform, dtype=np.float64).tobytes(),
+            float(camera.fovy), float(camera.aspect), float(camera.near),
+            int(camera.internal_width), int(camera.internal_height))
+
+
+def _cfg_key(cfg):
+    return (cfg.small_max_px, cfg.medium_max_px, cfg.tile_px, cfg.stage2_capacity,
+            cfg.stage3_capacity, bool(cfg.tiny_cull), cfg.force_stage, cfg.instancing)
+
+
+def _cached_frame(draw_list, camera, cfg, ctx, use_filter, work_range):
+    """A PreparedFrame for these inputs, reused across calls.  Entries hold
+    the draw list / context objects they were built from and match them by
+    identity (plus the item count and triangle total); the camera and the
+    config by value; the geometry by ``scene_geometry``'s identity check, so
+    re-assigned mesh arrays rebuild the frame.  At most 4 frames are kept."""
+    device = torch.device("cuda", torch.cuda.current_device())
+    key = (id(draw_list), id(ctx), _camera_key(camera), _cfg_key(cfg), use_filter,
+           None if work_range is None else (int(work_range[0]), int(work_range[1])), str(device))
+    ent = _frame_cache.get(key)
+    if ent is not None:
+        pf = ent
+        if (pf.draw_list is draw_list and (ctx is None or pf.ctx_arg is ctx)
+                and len(draw_list.items) == pf.n_items
+                and int(draw_list.total_triangles) == pf.total
+                and pf.geo is scene_geometry([pf.ctx.meshes[int(m)] for m in pf.mesh_ids],
+                                             device)):
+            pf.refresh(new_framebuffer=True)
+            return pf
+        _frame_cache.pop(key, None)
+    pf = PreparedFrame(draw_list, camera, cfg, ctx, device=device, use_filter=use_filter,
+                       work_range=work_range)
+    pf.ctx_arg = ctx
+    if len(_frame_cache) >= _FRAME_CACHE_MAX:
+        _frame_cache.pop(next(iter(_frame_cache)))
+    _frame_cache[key] = pf
+    return pf
+
+
 def render_draw_list(draw_list: DrawList, camera, cfg: RasterConfig | None = None,
                      ctx: RenderContext | None = None, *, use_filter=None,
                      work_range=None) -> tuple[Framebuffer, FrameStats]:
     """Run the three stages over a prebuilt draw list (pipeline.py:207-365).
 
-    The returned Framebuffer keeps its words in HBM (``device_words``);
-    ``.words`` downloads them as the reference's host ``np.uint64`` array."""
+    ``ctx`` may be this package's RenderContext or the reference's
+    (``trirast.pipeline.RenderContext``, see ``adopt_context``).  Repeated
+    calls with the same draw list, camera and config reuse the prepared
+    frame (descriptors re-uploaded, host setup skipped).  The returned
+    Framebuffer keeps its words in HBM (``device_words``); ``.words``
+    downloads them as the reference's host ``np.uint64`` array."""
     cfg = cfg or RasterConfig()
     width, height = camera.internal_width, camera.internal_height
     total = draw_list.total_triangles
     if total == 0:
         st = FrameStats(total_triangles=0, items=len(draw_list.items))
         return Framebuffer(width, height), st
-    frame = PreparedFrame(draw_list, camera, cfg, ctx, use_filter=use_filter,
-                          work_range=work_range)
+    frame = _cached_frame(draw_list, camera, cfg, ctx, use_filter, work_range)
     c, secs = frame.run()
     return Framebuffer(width, height, device_words=frame.fb), frame.stats(c, secs)
 

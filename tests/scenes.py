@@ -205,3 +205,19 @@ def stats_vector_from_frame(st):
                      s1.culled_tiny, s1.culled_backface, s1.culled_degenerate, s1.fragments,
                      s2.direct, s2.tiled, s2.dropped, s2.fragments, s2.tiles, s3.entries,
                      s3.fragments], dtype=np.int64)
+
+
+def compress_scene(scene):
+    """The same scene with QuantizedPositions + PackedIndexBuffer meshes
+    (geomcodec.py:65-120 encoders), decoded in-register on the GPU and on
+    the host by the oracle (configs Bq / Dq)."""
+    from paper_2604_21749_b200 import codec
+    out = []
+    for node in scene:
+        m = node.mesh
+        q = codec.quantize_positions(m.positions, m.aabb)
+        p = codec.compress_indices(m.indices)
+        cm = Mesh(positions=q, indices=p, triangle_count=m.triangle_count, aabb=m.aabb,
+                  vertex_colors=m.vertex_colors, name=m.name + "_q")
+        out.append(SceneNode(mesh=cm, transforms=node.transforms))
+    return out

@@ -322,3 +322,80 @@ def test_batched_cull_matches_per_instance_path():
         assert np.array_equal(np.asarray(a.instance_transform), b.transform)
     assert np.array_equal(dl.prefix_sums, ref.prefix)
     assert 0 < len(dl.items) < 1405
+
+
+# --------------------------------------------------------------------------
+# drop-in context and shard-local geometry (CPU: host logic only)
+
+def test_reference_render_context_is_adopted():
+    """render_draw_list(ctx=<trirast RenderContext>): the reference's flat
+    positions / indices become one mesh addressed through its item offsets,
+    and its matrices and prefix are used as given (pipeline.py:68-84)."""
+    from refctx import from_golden
+    from paper_2604_21749_b200.pipeline import adopt_context
+    for name in ("lantern_on", "random2024_005", "classifier"):
+        g = load_golden(name)
+        scene = golden_scene(g, compressed=False)
+        cam = golden_camera(g)
+        dl = build_draw_list(scene, cam)
+        ref = from_golden(g)
+        ctx = adopt_context(ref, dl, cam)
+        assert len(ctx.meshes) == 1
+        m = ctx.meshes[0]
+        assert np.array_equal(m.positions, g["ctx_positions"])
+        assert np.array_equal(m.indices, g["ctx_indices"])
+        assert np.array_equal(ctx.item_vtx_off, g["item_vtx_off"])
+        assert np.array_equal(ctx.item_idx_off, g["item_idx_off"])
+        assert np.array_equal(ctx.item_mv, g["item_mv"])
+        assert np.array_equal(ctx.prefix, g["prefix"])
+        assert np.array_equal(ctx.group_prefix, g["group_prefix"])
+        assert np.array_equal(ctx.group_items, g["group_items"])
+        assert (ctx.item_mesh == 0).all()
+        # cached on the context object: the same flat mesh next time
+        assert adopt_context(ref, dl, cam).meshes[0] is m
+    with pytest.raises(TypeError, match="RenderContext"):
+        adopt_context(object(), dl, cam)
+
+
+def test_shard_items_select_only_the_ranks_geometry():
+    """A rank's work range touches only its items: PreparedFrame uploads
+    only those items' meshes (each GPU holds its shard)."""
+    from paper_2604_21749_b200.distributed import shard_range
+    from paper_2604_21749_b200.pipeline import build_context, shard_items
+    from paper_2604_21749_b200 import generators as gen
+    # 6 distinct meshes, one node each (flat work space)
+    nodes = []
+    for k in range(6):
+        m = gen.make_tessellated_quad(4 + k)
+        T = np.eye(4)
+        T[0, 3] = 1.5 * k - 4.0
+        nodes.append(SceneNode(mesh=m, transforms=[T]))
+    cam = Camera.look_at((0.0, 0.0, 9.0), (0.0, 0.0, 0.0), width=320, height=120)
+    dl = build_draw_list(nodes, cam)
+    ctx = build_context(dl, cam)
+    assert len(ctx.meshes) == 6
+    total = dl.total_triangles
+    seen = np.zeros(6, dtype=int)
+    for world in (2, 3):
+        for r in range(world):
+            lo, hi = shard_range(total, world, r)
+            mask = shard_items(ctx, (lo, hi), False)
+            s, e = ctx.prefix[:-1], ctx.prefix[1:]
+            want = (e > lo) & (s < hi)
+            assert np.array_equal(mask, want)
+            used = np.unique(ctx.item_mesh[mask])
+            assert len(used) < 6                         # never the whole scene
+            seen[used] += 1
+    assert (seen > 0).all()
+    # instanced work space: whole groups (all instances of a node)
+    lg = gen.make_lantern_grid(3, 2, tris_per_mesh=200, spacing=1.8)
+    extra = SceneNode(mesh=gen.make_tessellated_quad(10), transforms=[np.eye(4)])
+    cam = Camera.look_at((0.0, 6.0, 9.0), (0.0, 0.0, 0.0), width=160, height=120)
+    dl = build_draw_list(lg + [extra], cam)
+    ctx = build_context(dl, cam)
+    g0 = int(ctx.group_prefix[1])
+    m0 = shard_items(ctx, (0, g0), True)
+    assert m0.sum() == ctx.group_item_count[0]
+    assert len(np.unique(ctx.item_mesh[m0])) == 1
+    m1 = shard_items(ctx, (g0, int(ctx.group_prefix[-1])), True)
+    assert not (m0 & m1).any() and (m0 | m1).all()

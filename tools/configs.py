@@ -22,21 +22,9 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import paper_2604_21749_b200 as cr  # noqa: E402
-from paper_2604_21749_b200 import codec  # noqa: E402
 from paper_2604_21749_b200 import generators as gen  # noqa: E402
 from paper_2604_21749_b200.pipeline import PreparedFrame  # noqa: E402
-
-
-def compress_scene(scene):
-    out = []
-    for node in scene:
-        m = node.mesh
-        q = codec.quantize_positions(m.positions, m.aabb)
-        p = codec.compress_indices(m.indices)
-        cm = cr.Mesh(positions=q, indices=p, triangle_count=m.triangle_count, aabb=m.aabb,
-                     vertex_colors=m.vertex_colors, name=m.name + "_q")
-        out.append(cr.SceneNode(mesh=cm, transforms=node.transforms))
-    return out
+from scenes import compress_scene  # noqa: E402
 
 
 def build(name):
