@@ -36,13 +36,14 @@
 extern "C" {
 #endif
 
-#define CURAST_ABI_VERSION 1
+#define CURAST_ABI_VERSION 2
 
 enum curast_pos_format {
     CURAST_POS_F64 = 0,   /* double[V][3] (reference ctx.positions)            */
     CURAST_POS_F32 = 1,   /* float[V][4] (x, y, z, 0), values exactly f32: one
                              128-bit load per vertex gather                    */
-    CURAST_POS_U16 = 2    /* uint16[V][3] + per-item grid (geomcodec.py:87-101) */
+    CURAST_POS_U16 = 2    /* uint16[V][4] (x, y, z, 0) + per-item grid
+                             (geomcodec.py:87-101): one 64-bit load per vertex */
 };
 enum curast_idx_format {
     CURAST_IDX_U32 = 0,   /* uint32 stream (reference ctx.indices)             */
@@ -63,10 +64,7 @@ enum curast_counter {
     CURAST_C_EXACT = 19,      /* stage-1 triangles decided by the fp64 path     */
     CURAST_C_QX = 20,         /* fp64 work-queue entries (counts past capacity) */
     CURAST_C_CLAIM1I = 21,    /* instanced-table claim counter (internal)       */
-    CURAST_C_SLICE_CLAIM = 22,/* 4 slots: claim counters of stage-1 slices      */
-    CURAST_C_SLICE_SNAP = 26, /* 4 slots: fp64-queue size after each slice      */
-    CURAST_C_PROVED = 30,     /* fp64-queue entries decided by the fp32 prover  */
-    CURAST_C_CLAIM1B = 31,    /* second flat-table claim counter (die halves)   */
+                              /* 22-31 reserved                                 */
     CURAST_C_QXHOLES = 32,    /* fp64-queue slots reserved but left empty       */
     CURAST_COUNTER_SLOTS = 40
 };
@@ -88,17 +86,15 @@ enum curast_error {
  * covering instances [first, first + CURAST_INST_BLOCK) of the group */
 #define CURAST_INST_BLOCK 16
 
-/* meshlets: triangles per meshlet (a strip of 63 quads has 128 vertices),
- * bytes per meshlet triangle record (3 u8 per triangle, padded), largest
- * vertex list with u8 slot indices: vertex j of the list is stored in the
- * kernel's shared-memory slot j + j/16 (one pad slot per 16 keeps the
- * lookups of strip meshes bank-conflict free), and the u8 triangle record
- * holds that slot number */
 /* fp64-queue slots a stage-1 warp reserves at a time (holes: tag -1) */
 #define CURAST_QX_RES 128
-#define CURAST_MESHLET_TRIS 126
-#define CURAST_MESHLET_BYTES 384
-#define CURAST_MESHLET_MAX_VERTS 240
+/* queue tags: item << 40 | local; bit 62 set = the producer proved the
+ * triangle's vertices in front of the near plane and inside the viewport
+ * (k_s1_exact then skips those tests); items < 2^22 */
+#define CURAST_QX_INTERIOR (1ll << 62)
+/* triangles per stage-1 warp step (32 lanes x 4) and per lane-major index
+ * step (indices_ilv) */
+#define CURAST_STEP_TRIS 128
 
 /* fp64 work-queue entry: 6 int64 words (48 B) */
 #define CURAST_QX_WORDS 6
@@ -119,33 +115,15 @@ typedef struct curast_frame {
     const float *item_filter;         /* float[n_items][16] or NULL           */
     const double *item_qgrid;         /* U16: double[n_items][6] gmin, gsize  */
     const int64_t *item_pack;         /* PACKED: int64[n_items][2] min, bits  */
-    /* ---- meshlets of u32 index streams (optional: NULL = none) ----
-     * triangle t of a mesh lies in meshlet t / CURAST_MESHLET_TRIS; a meshlet
-     * lists its unique vertices (ascending mesh-local ids) and stores each
-     * triangle as 3 u8 slot numbers (vertex j -> slot j + j/16).  A meshlet with more than
-     * CURAST_MESHLET_MAX_VERTS vertices has no u8 form: its triangles are
-     * read from the index stream instead.                                  */
-    const int64_t *item_ml_off;       /* first meshlet of the item's mesh     */
-    const int64_t *ml_voff;           /* int64[n_meshlets+1] into ml_verts    */
-    const uint32_t *ml_verts;         /* mesh-local vertex ids                */
-    const uint8_t *ml_tris;           /* uint8[n_meshlets][CURAST_MESHLET_BYTES] */
     /* ---- lane-major index steps (POS_F32 + IDX_U32; optional) ----
-     * the u32 stream re-laid out per step of CURAST_MESHLET_TRIS triangles:
+     * the u32 stream re-laid out per step of CURAST_STEP_TRIS triangles:
      * 384 words, lane l's 12 words = triangles l, l+32, l+64, l+96 of the
-     * step (3 indices each, zero padded past the step).  One 3 x 128-bit
+     * step (3 indices each, zero padded past the mesh).  One 3 x 128-bit
      * load per lane, and each vertex gather of the warp then reads 32
      * consecutive triangles' vertices (fewer L1 lines than 4 consecutive
      * triangles per lane).                                                  */
     const int64_t *item_ilv_off;      /* word offset of the item's mesh       */
     const uint32_t *indices_ilv;
-    /* ---- per-chunk object-space boxes (POS_F32 + IDX_U32; optional) ----
-     * box b of a mesh bounds the vertices of its triangles
-     * [b*C, (b+1)*C), C = curast_chunk_tris(0): float[8] = min xyz, 0,
-     * max xyz, 0.  Stage 1 projects a chunk's box corners once and takes
-     * the per-triangle fast path when the whole chunk is provably in front
-     * of the near margin and inside the viewport.                          */
-    const int64_t *item_cb_off;       /* first box of the item's mesh         */
-    const float *chunk_box;           /* float[n_boxes][8]                    */
     /* ---- instancing groups (pipeline.py:114-135) ---- */
     int32_t instanced;                /* 1: stage1_instanced_range semantics  */
     int32_t use_filter;               /* 1: fp32 cull filter + fp64 fallback  */

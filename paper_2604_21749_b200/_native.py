@@ -11,25 +11,22 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcurast_b200.so")
-ABI_VERSION = 1
+LIB_PATH = os.environ.get("CURAST_LIB") or os.path.join(_HERE, "libcurast_b200.so")
+ABI_VERSION = 2
 
 POS_F64, POS_F32, POS_U16 = 0, 1, 2
 IDX_U32, IDX_PACKED = 0, 1
 
 C_Q2, C_Q3, C_S1, C_S2, C_S3 = 0, 1, 2, 10, 15
 C_CLAIM1, C_CLAIM2, C_CLAIM3, C_EXACT, C_QX = 16, 17, 18, 19, 20
-C_PROVED = 30
 QX_RES = 128       # CURAST_QX_RES: fp64-queue slots a stage-1 warp reserves at a time
 C_QXHOLES = 32     # fp64-queue slots reserved by a warp but left empty (tag -1)
 COUNTER_SLOTS = 40
 FILTER_FLOATS = 16
 INST_BLOCK = 16          # CURAST_INST_BLOCK: instances per instanced work unit
 QX_WORDS = 6
-MESHLET_TRIS = 126       # CURAST_MESHLET_TRIS
-MESHLET_BYTES = 384      # CURAST_MESHLET_BYTES
-MESHLET_MAX_VERTS = 240  # CURAST_MESHLET_MAX_VERTS (u8 slot j + j//16)
-S1_CHUNK = 16 * MESHLET_TRIS   # curast_chunk_tris(0): flat stage-1 chunk
+STEP_TRIS = 128          # CURAST_STEP_TRIS: triangles per warp step / index step
+S1_CHUNK = 16 * STEP_TRIS      # curast_chunk_tris(0): flat stage-1 chunk
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -46,9 +43,7 @@ class CurastFrame(ctypes.Structure):
         ("n_items", _I64), ("prefix", _P), ("item_mv", _P), ("item_mw", _P),
         ("item_vtx_off", _P), ("item_idx_off", _P), ("item_filter", _P),
         ("item_qgrid", _P), ("item_pack", _P),
-        ("item_ml_off", _P), ("ml_voff", _P), ("ml_verts", _P), ("ml_tris", _P),
         ("item_ilv_off", _P), ("indices_ilv", _P),
-        ("item_cb_off", _P), ("chunk_box", _P),
         ("instanced", _I32), ("use_filter", _I32),
         ("n_groups", _I64), ("group_prefix", _P), ("group_item_off", _P),
         ("group_item_count", _P), ("group_items", _P),

@@ -1,0 +1,322 @@
+// stage1_v2.cuh — the streamed stage-1 cull filter (f32 positions, u32
+// indices): per-vertex projection sharing and a per-lane error bound.
+//
+// A lane owns 4 consecutive triangles of a 128-triangle warp step (3 x
+// 128-bit index loads).  When the whole warp's index runs are quad-strip
+// runs — (a,c,b),(b,c,d) (make_tessellated_quad) or (a,b,c),(b,d,c)
+// (make_sphere) — the lane's 12 vertex refs name 6 distinct vertices: each
+// is gathered and projected ONCE (6 LDG.128 + 6 projections instead of 12).
+// The filter bound eps (filter.cuh) grows with max|p'| and 1/min d', so one
+// eps over the lane's vertices bounds all four triangles; when every lane's
+// vertex box lies provably inside the viewport and in front of the near
+// margin (the warp-uniform common case) only the tiny cull is left to decide
+// per triangle, else the full decision (lean_decide) runs.  Decisions are a
+// subset of the fp64 path's (CULL_FRUSTUM / CULL_TINY proven with the
+// rigorous bound), so the output is bit-identical to the all-fp64 path.
+//
+// Undecided triangles go to the global fp64 queue (48-byte entries with
+// their positions, one reservation per 128 slots, qxres.cuh) for k_s1_exact.
+#pragma once
+#include "exact.cuh"
+#include "filter.cuh"
+#include "qxres.cuh"
+
+namespace curast {
+
+// One projected vertex (filter units): P = (X', Y') / d', D = d'.
+struct PV {
+    float2 P;
+    float D;
+};
+
+__device__ __forceinline__ PV pv_project(const LeanConsts &F, const float4 &q) {
+    PV v;
+    v.D = __fmaf_rn(F.dz, q.z, __fmaf_rn(F.dy, q.y, __fmaf_rn(F.dx, q.x, F.d3)));
+    float2 t = __ffma2_rn(F.cx, make_float2(q.x, q.x), F.c3);
+    t = __ffma2_rn(F.cy, make_float2(q.y, q.y), t);
+    t = __ffma2_rn(F.cz, make_float2(q.z, q.z), t);
+    const float r = rcp_approx(v.D);
+    v.P = __fmul2_rn(t, make_float2(r, r));
+    return v;
+}
+
+// Lane bound over NV projected vertices: eps as filter.cuh / lean_bits_v
+// with M = max |p'| and dmin = min d' over all of them (eps is monotone in
+// both, so it bounds each of the lane's triangles), the lane's vertex box,
+// and whether that box is provably interior (no frustum / near decision).
+struct LaneB {
+    float eps, e2, lo5, hi5;
+    bool near_ok, interior;
+};
+
+template <int NV>
+__device__ __forceinline__ LaneB lane_bound(const LeanConsts &F, const PV *v, float W, float H,
+                                            float slack) {
+    float dmin = v[0].D, mnx = v[0].P.x, mxx = v[0].P.x, mny = v[0].P.y, mxy = v[0].P.y;
+#pragma unroll
+    for (int k = 1; k < NV; ++k) {
+        dmin = fminf(dmin, v[k].D);
+        mnx = fminf(mnx, v[k].P.x);
+        mxx = fmaxf(mxx, v[k].P.x);
+        mny = fminf(mny, v[k].P.y);
+        mxy = fmaxf(mxy, v[k].P.y);
+    }
+    LaneB b;
+    const float M = fmaxf(fmaxf(fabsf(mnx), fabsf(mxx)), fmaxf(fabsf(mny), fabsf(mxy)));
+    float eps = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(dmin);
+    eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, slack));
+    b.eps = eps;
+    b.e2 = eps + eps;
+    b.lo5 = eps + 0.5f;
+    b.hi5 = eps - 0.5f;
+    b.near_ok = dmin > F.near_hi;
+    b.interior = b.near_ok && (mnx - eps > 0.0f) && (mny - eps > 0.0f) && (mxx + eps < W) &&
+                 (mxy + eps < H);
+    return b;
+}
+
+// Tiny-cull decision of an interior triangle (every frustum / near /
+// offscreen outcome provably false except a zero extent): 1 = fp64 needed.
+__device__ __forceinline__ unsigned tri_fast(const PV &a, const PV &b, const PV &c, const LaneB &L,
+                                             bool tiny) {
+    const float mnx = fminf(a.P.x, fminf(b.P.x, c.P.x)), mxx = fmaxf(a.P.x, fmaxf(b.P.x, c.P.x));
+    const float mny = fminf(a.P.y, fminf(b.P.y, c.P.y)), mxy = fmaxf(a.P.y, fmaxf(b.P.y, c.P.y));
+    const float2 ext = __fadd2_rn(make_float2(mxx, mxy), make_float2(-mnx, -mny));
+    const float2 lo = __fadd2_rn(make_float2(mnx, mny), make_float2(-L.lo5, -L.lo5));
+    const float2 hi = __fadd2_rn(make_float2(mxx, mxy), make_float2(L.hi5, L.hi5));
+    const bool e = (ext.x > L.e2) && (ext.y > L.e2);
+    const bool t = (ceilf(lo.x) > hi.x) || (ceilf(lo.y) > hi.y);
+    return (tiny && e && t) ? 0u : 1u;
+}
+
+// Full decision (lean_decide) under the lane bound: bit 0 fp64, bit 1 frustum.
+__device__ __forceinline__ unsigned tri_full(const PV &a, const PV &b, const PV &c, const LaneB &L,
+                                             float W, float H, bool tiny) {
+    const float mnx = fminf(a.P.x, fminf(b.P.x, c.P.x)), mxx = fmaxf(a.P.x, fmaxf(b.P.x, c.P.x));
+    const float mny = fminf(a.P.y, fminf(b.P.y, c.P.y)), mxy = fmaxf(a.P.y, fmaxf(b.P.y, c.P.y));
+    const float lox = mnx - L.eps, loy = mny - L.eps, hix = mxx + L.eps, hiy = mxy + L.eps;
+    const bool interior = lox > 0.0f && loy > 0.0f && hix < W && hiy < H;
+    const float e4 = 4.0f * L.eps;
+    const bool ext = (hix - lox > e4) && (hiy - loy > e4);
+    const bool tx = ceilf(lox - 0.5f) > hix - 0.5f;
+    const bool ty = ceilf(loy - 0.5f) > hiy - 0.5f;
+    const bool is_tiny = L.near_ok && interior && tiny && ext && (tx || ty);
+    const bool is_fr = L.near_ok && !interior && (hix < 0.0f || hiy < 0.0f || lox > W || loy > H);
+    return (is_tiny || is_fr) ? (is_fr ? 2u : 0u) : 1u;
+}
+
+// Vertex-ref patterns of a lane's 4 triangles (refs 3t..3t+2):
+//   0 generic: 12 gathered vertices, triangle t = (3t, 3t+1, 3t+2)
+//   1 grid quads (a,c,b),(b,c,d): distinct refs 0,1,2,5,8,11 = U0..U5,
+//     triangles (U0,U1,U2) (U2,U1,U3) (U2,U3,U4) (U4,U3,U5)
+//   2 sphere quads (a,b,c),(b,d,c): distinct refs 0,1,2,4,7,10,
+//     triangles (U0,U1,U2) (U1,U3,U2) (U1,U4,U3) (U4,U5,U3)
+// (each triangle's vertex order is irrelevant: the bbox tests are symmetric)
+__device__ __forceinline__ int strip_kind(const uint32_t *ix, bool full) {
+    const bool gq = full && ix[3] == ix[2] && ix[4] == ix[1] && ix[6] == ix[2] &&
+                    ix[7] == ix[5] && ix[9] == ix[8] && ix[10] == ix[5];
+    const bool sq = full && ix[3] == ix[1] && ix[5] == ix[2] && ix[6] == ix[1] &&
+                    ix[8] == ix[4] && ix[9] == ix[7] && ix[11] == ix[4];
+    return __all_sync(0xffffffffu, gq) ? 1 : (__all_sync(0xffffffffu, sq) ? 2 : 0);
+}
+
+// Distinct vertex refs of a strip lane (strip_r) and its triangles' vertex
+// slots (strip_g: reference k = 3t + e -> slot among the 6 distinct ones).
+__host__ __device__ constexpr int strip_r(int kind, int k) {
+    return k < 3 ? k : (kind == 1 ? 3 * k - 4 : 3 * k - 5);
+}
+__host__ __device__ constexpr int strip_g(int kind, int k) {
+    // kind 1: 0 1 2 | 2 1 3 | 2 3 4 | 4 3 5    kind 2: 0 1 2 | 1 3 2 | 1 4 3 | 4 5 3
+    return kind == 1 ? (k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 2 : k == 4 ? 1 :
+                        k == 5 ? 3 : k == 6 ? 2 : k == 7 ? 3 : k == 8 ? 4 : k == 9 ? 4 :
+                        k == 10 ? 3 : 5)
+                     : (k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 1 : k == 4 ? 3 :
+                        k == 5 ? 2 : k == 6 ? 1 : k == 7 ? 4 : k == 8 ? 3 : k == 9 ? 4 :
+                        k == 10 ? 5 : 3);
+}
+static_assert(strip_r(1, 3) == 5 && strip_r(1, 5) == 11 && strip_r(2, 3) == 4 &&
+              strip_r(2, 5) == 10, "strip refs");
+
+// The 4 decisions of a strip lane (6 distinct vertices, each gathered and
+// projected once, one lane bound): need bits in bits 0-3, frustum bits in
+// bits 4-7, bit 8 = the lane's vertices are provably in front of the near
+// plane and inside the viewport (CURAST_QX_INTERIOR for its queue entries).
+template <int KIND>
+__device__ __forceinline__ unsigned lane_decide_strip(const LeanConsts &F,
+                                                      const float4 *__restrict__ pb,
+                                                      const uint32_t *ix, float W, float H,
+                                                      float slack, bool tiny) {
+    PV v[6];
+    {
+        float4 q[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) q[k] = __ldg(pb + ix[strip_r(KIND, k)]);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] = pv_project(F, q[k]);
+    }
+    const LaneB L = lane_bound<6>(F, v, W, H, slack);
+    unsigned bits = L.interior ? 0x100u : 0u;
+    if (__all_sync(0xffffffffu, L.interior)) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            bits |= tri_fast(v[strip_g(KIND, 3 * t)], v[strip_g(KIND, 3 * t + 1)],
+                             v[strip_g(KIND, 3 * t + 2)], L, tiny) << t;
+    } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const unsigned b = tri_full(v[strip_g(KIND, 3 * t)], v[strip_g(KIND, 3 * t + 1)],
+                                        v[strip_g(KIND, 3 * t + 2)], L, W, H,
+                                        tiny);
+            bits |= ((b & 1u) << t) | ((b >> 1) << (4 + t));
+        }
+    }
+    return bits;
+}
+
+// Generic lane (no strip pattern): triangle by triangle, 3 gathers and a
+// per-triangle bound each (lean_bits), so only one triangle's vertices are
+// live at a time.
+__device__ __forceinline__ unsigned lane_decide_generic(const LeanConsts &F,
+                                                        const float4 *__restrict__ pb,
+                                                        const uint32_t *ix, float W, float H,
+                                                        float slack, bool tiny) {
+    unsigned bits = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const float4 a = __ldg(pb + ix[3 * t]), b = __ldg(pb + ix[3 * t + 1]),
+                     c = __ldg(pb + ix[3 * t + 2]);
+        const float x[3] = {a.x, b.x, c.x}, y[3] = {a.y, b.y, c.y}, z[3] = {a.z, b.z, c.z};
+        const unsigned r = lean_bits(F, x, y, z, W, H, slack, tiny);
+        bits |= ((r & 1u) << t) | ((r >> 1) << (4 + t));
+    }
+    return bits;
+}
+
+__device__ __forceinline__ unsigned lane_decide(int kind, const LeanConsts &F,
+                                                const float4 *__restrict__ pb, const uint32_t *ix,
+                                                float W, float H, float slack, bool tiny) {
+    if (kind == 1) return lane_decide_strip<1>(F, pb, ix, W, H, slack, tiny);
+    if (kind == 2) return lane_decide_strip<2>(F, pb, ix, W, H, slack, tiny);
+    return lane_decide_generic(F, pb, ix, W, H, slack, tiny);
+}
+
+// The warp's 128-triangle step at chunk offset s0: indices of triangles
+// o .. o+3 (o = s0 + 4 lane) into ix[12]; nv valid triangles.
+__device__ __forceinline__ void load_step_indices(const uint32_t *__restrict__ ib, int o, int nv,
+                                                  bool vec, uint32_t *ix) {
+    if (vec && nv == 4) {
+        const uint4 *v = (const uint4 *)(ib + 3 * o);
+        const uint4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
+        ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w;
+        ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
+        ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 12; ++k) ix[k] = (k < 3 * nv) ? __ldg(ib + 3 * o + k) : 0u;
+    }
+}
+
+// warp claim of the next flat-table chunk (lane 0), broadcast
+__device__ __forceinline__ bool claim_flat(const curast_frame_t &f, int lane, int64_t total,
+                                           long long &item, long long &lo, long long &hi) {
+    long long c = 0;
+    if (lane == 0) {
+        c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1), 1ull);
+        if (c < total) {
+            const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
+            item = __ldg(f.unit_index + u);
+            lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * kS1Chunk;
+            hi = __ldg(f.unit_hi + u);
+            hi = lo + kS1Chunk < hi ? lo + kS1Chunk : hi;
+        }
+    }
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= total) return false;
+    item = __shfl_sync(0xffffffffu, item, 0);
+    lo = __shfl_sync(0xffffffffu, lo, 0);
+    hi = __shfl_sync(0xffffffffu, hi, 0);
+    return true;
+}
+
+// ------------------------------------------------ filter -> global fp64 queue
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
+    constexpr int STEP = 128;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    unsigned cnt16 = 0;   // frustum | tiny << 16
+    const float W = (float)f.width, H = (float)f.height;
+    const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
+    const bool tiny = f.tiny_cull != 0;
+    const int64_t total = __ldg(f.unit_chunk_prefix + f.n_units);
+    unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+    __shared__ QxReserve sres[8];
+    QxReserve &R = sres[threadIdx.x >> 5];
+    if (lane == 0) R = QxReserve{0u, 0};
+    __syncwarp();
+    for (;;) {
+        long long item = 0, lo = 0, hi = 0;
+        if (!claim_flat(f, lane, total, item, lo, hi)) break;
+        if (__any_sync(0xffffffffu, cnt16 & 0x80008000u)) {
+            unsigned long long cnt[2] = {cnt16 & 0xffffu, cnt16 >> 16};
+            flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+            flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+            cnt16 = 0;
+        }
+        LeanConsts F;
+        lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);
+        const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + item);
+        const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + item) + 3 * lo;
+        const int n = (int)(hi - lo);
+        const bool vec = (((uintptr_t)ib) & 15) == 0;
+        const long long tag = (item << 40) | lo;
+        for (int s0 = 0; s0 < n; s0 += STEP) {
+            const int o = s0 + 4 * lane;
+            const int nv = max(0, min(4, n - o));
+            uint32_t ix[12];
+            load_step_indices(ib, o, nv, vec, ix);
+            const int kind = strip_kind(ix, nv == 4);
+            const unsigned bits = lane_decide(kind, F, pb, ix, W, H, slack, tiny);
+            const unsigned vmask = (1u << nv) - 1u;
+            const unsigned need = bits & vmask, fr = (bits >> 4) & vmask;
+            cnt16 += (unsigned)__popc(fr) + ((unsigned)(nv - __popc(need) - __popc(fr)) << 16);
+            unsigned b[4];
+            int tot = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                b[t] = __ballot_sync(0xffffffffu, (need >> t) & 1u);
+                tot += __popc(b[t]);
+            }
+            if (tot) {
+                const QxSlots qs = qx_reserve(R, qcount, tot, lane);
+                int base = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if ((need >> t) & 1u) {
+                        const long long slot = qs.at(base + __popc(b[t] & lt_mask));
+                        if (slot < f.qx_cap) {
+                            int64_t *e = f.qx + CURAST_QX_WORDS * slot;
+                            // the entry's positions: re-read (L1 hits) for
+                            // the few queued triangles instead of keeping
+                            // every gathered vertex live
+                            const float4 va = __ldg(pb + ix[3 * t]), vb = __ldg(pb + ix[3 * t + 1]),
+                                         vc = __ldg(pb + ix[3 * t + 2]);
+                            *(float4 *)e = make_float4(va.x, va.y, va.z, vb.x);
+                            *(float4 *)(e + 2) = make_float4(vb.y, vb.z, vc.x, vc.y);
+                            *(float2 *)(e + 4) = make_float2(vc.z, 0.0f);
+                            e[CURAST_QX_TAG] =
+                                (tag + o + t) | ((bits & 0x100u) ? CURAST_QX_INTERIOR : 0ll);
+                        }
+                    }
+                    base += __popc(b[t]);
+                }
+            }
+        }
+    }
+    qx_reserve_close(f, R, lane);
+    unsigned long long cnt[2] = {cnt16 & 0xffffu, cnt16 >> 16};
+    flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+    flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+}
+
+}  // namespace curast

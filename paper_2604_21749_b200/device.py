@@ -150,25 +150,11 @@ class DeviceMesh:
             return g[:3] + (q + 0.5) / 65536.0 * g[3:]
         raise ValueError("unsupported position conversion")
 
-    def meshlets(self):
-        """(ml_voff int64[nm+1], ml_verts int32[], ml_tris uint8[nm*3*MT]) of
-        this mesh's u32 index stream, built once on the device (cached)."""
-        if getattr(self, "_meshlets", None) is None:
-            self._meshlets = build_meshlets(self.indices_u32(), self.triangle_count)
-        return self._meshlets
-
     def index_steps(self):
         """Lane-major index steps of the u32 stream (built once)."""
         if getattr(self, "_index_steps", None) is None:
             self._index_steps = build_index_steps(self.indices_u32(), self.triangle_count)
         return self._index_steps
-
-    def chunk_boxes(self):
-        """Per-chunk object-space boxes (POS_F32 meshes), built once."""
-        if getattr(self, "_chunk_boxes", None) is None:
-            self._chunk_boxes = build_chunk_boxes(self.positions, self.indices_u32(),
-                                                  self.triangle_count)
-        return self._chunk_boxes
 
     def indices_u32(self):
         if self.idx_format == N.IDX_U32:
@@ -185,52 +171,11 @@ class DeviceMesh:
         return (rel + mn).to(torch.int64).to(torch.int32)
 
 
-def build_meshlets(indices: torch.Tensor, triangle_count: int, block: int = 1 << 16):
-    """Meshlets of a u32 index stream (curast.h CURAST_MESHLET_TRIS).
-
-    Meshlet m holds triangles [m*MT, (m+1)*MT) in stream order (global
-    triangle IDs stay implicit); its unique vertex ids ascending, and every
-    triangle as 3 u8 slot numbers (entry j -> slot j + j//16).  A meshlet with more than
-    CURAST_MESHLET_MAX_VERTS unique vertices keeps a count above the limit and
-    no valid u8 data (the kernel reads the index stream for it)."""
-    MT, MB = N.MESHLET_TRIS, N.MESHLET_BYTES
-    dev = indices.device
-    T = int(triangle_count)
-    nm = -(-T // MT)
-    if nm == 0:
-        return (torch.zeros(1, dtype=torch.int64, device=dev),
-                torch.zeros(0, dtype=torch.int32, device=dev),
-                torch.zeros(0, dtype=torch.uint8, device=dev))
-    ix = indices[:3 * T].to(torch.int64) & 0xFFFFFFFF
-    pad = nm * 3 * MT - 3 * T
-    if pad:
-        ix = torch.cat([ix, ix[-1:].expand(pad)])
-    rows = ix.view(nm, 3 * MT)
-    counts, verts, tris = [], [], []
-    for b0 in range(0, nm, block):
-        r = rows[b0:b0 + block]
-        srt, _ = torch.sort(r, dim=1)
-        new = torch.ones_like(srt, dtype=torch.bool)
-        new[:, 1:] = srt[:, 1:] != srt[:, :-1]
-        rank = torch.cumsum(new, dim=1) - 1
-        loc = torch.gather(rank, 1, torch.searchsorted(srt, r))
-        counts.append(new.sum(dim=1))
-        verts.append(srt[new].to(torch.int32))
-        t8 = torch.zeros((r.shape[0], MB), dtype=torch.uint8, device=dev)
-        # u8 shared-memory slot of list entry j: j + j // 16 (curast.h)
-        t8[:, :3 * MT] = (loc + loc // 16).clamp_(max=255).to(torch.uint8)
-        tris.append(t8.reshape(-1))
-    nu = torch.cat(counts)
-    voff = torch.zeros(nm + 1, dtype=torch.int64, device=dev)
-    voff[1:] = torch.cumsum(nu, 0)
-    return voff, torch.cat(verts), torch.cat(tris)
-
-
 def build_index_steps(indices: torch.Tensor, triangle_count: int) -> torch.Tensor:
-    """Lane-major index steps (curast.h indices_ilv): per step of MT
-    triangles 384 words, lane l holding triangles l + 32k (k < 4, zero padded
-    past the step) as 3 consecutive indices each."""
-    MT = N.MESHLET_TRIS
+    """Lane-major index steps (curast.h indices_ilv): per step of
+    CURAST_STEP_TRIS = 128 triangles 384 words, lane l holding triangles
+    l + 32k (k < 4, zero padded past the mesh) as 3 consecutive indices each."""
+    MT = N.STEP_TRIS
     T = int(triangle_count)
     ns = -(-T // MT)
     dev = indices.device
@@ -238,32 +183,7 @@ def build_index_steps(indices: torch.Tensor, triangle_count: int) -> torch.Tenso
         return torch.zeros(0, dtype=torch.int32, device=dev)
     x = torch.zeros((ns * MT, 3), dtype=torch.int32, device=dev)
     x[:T] = indices[:3 * T].view(T, 3)
-    x = torch.cat([x.view(ns, MT, 3), torch.zeros((ns, 128 - MT, 3), dtype=torch.int32,
-                                                  device=dev)], dim=1)
     return x.view(ns, 4, 32, 3).permute(0, 2, 1, 3).contiguous().view(-1)
-
-
-def build_chunk_boxes(pos4: torch.Tensor, indices: torch.Tensor, triangle_count: int,
-                      block: int = 1 << 12):
-    """float32[nb, 8] object-space boxes (min xyz, 0, max xyz, 0) of the
-    vertices of triangles [b*C, (b+1)*C), C = the flat stage-1 chunk."""
-    C = N.S1_CHUNK
-    dev = pos4.device
-    T = int(triangle_count)
-    nb = -(-T // C)
-    out = torch.zeros((nb, 8), dtype=torch.float32, device=dev)
-    if nb == 0:
-        return out
-    ix = indices[:3 * T].to(torch.int64) & 0xFFFFFFFF
-    pad = nb * 3 * C - 3 * T
-    if pad:
-        ix = torch.cat([ix, ix[-1:].expand(pad)])
-    rows = ix.view(nb, 3 * C)
-    for b0 in range(0, nb, block):
-        p = pos4[rows[b0:b0 + block], :3]                      # (b, 3C, 3)
-        out[b0:b0 + block, 0:3] = p.amin(dim=1)
-        out[b0:b0 + block, 4:7] = p.amax(dim=1)
-    return out
 
 
 _CACHE_ATTR = "_curast_device_copies"
@@ -338,38 +258,6 @@ class SceneGeometry:
         # lane-major index steps (built on first use, SceneGeometry.index_steps)
         self.ilv_off = [0] * len(dms)
         self.indices_ilv = None
-        # chunk boxes feed the chunk-class fast path of the meshlet kernel
-        self.cb_off = [0] * len(dms)
-        self.chunk_box = None
-        if (self.pos_format == N.POS_F32 and self.idx_format == N.IDX_U32
-                and os.environ.get("CURAST_MESHLETS", "0") == "1"):
-            parts, nb = [], 0
-            for k, d in enumerate(dms):
-                b = d.chunk_boxes()
-                self.cb_off[k] = nb
-                parts.append(b)
-                nb += b.shape[0]
-            self.chunk_box = parts[0] if len(parts) == 1 else torch.cat(parts)
-        # meshlets feed the f32 / u32 meshlet stage-1 kernel (CURAST_MESHLETS=1;
-        # the per-triangle kernel is the measured default)
-        self.ml_off = [0] * len(dms)
-        self.ml_voff = self.ml_verts = self.ml_tris = None
-        if (self.pos_format == N.POS_F32 and self.idx_format == N.IDX_U32
-                and os.environ.get("CURAST_MESHLETS", "0") == "1"):
-            vo_parts, vt_parts, tr_parts = [], [], []
-            nm = nvl = 0
-            for k, d in enumerate(dms):
-                voff, verts, tris = d.meshlets()
-                self.ml_off[k] = nm
-                vo_parts.append(voff[:-1] + nvl)
-                vt_parts.append(verts)
-                tr_parts.append(tris)
-                nm += voff.numel() - 1
-                nvl += verts.numel()
-            vo_parts.append(torch.full((1,), nvl, dtype=torch.int64, device=device))
-            self.ml_voff = torch.cat(vo_parts)
-            self.ml_verts = vt_parts[0] if len(vt_parts) == 1 else torch.cat(vt_parts)
-            self.ml_tris = tr_parts[0] if len(tr_parts) == 1 else torch.cat(tr_parts)
         self.keepalive = dms
 
     def index_steps(self):

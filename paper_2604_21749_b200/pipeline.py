@@ -263,8 +263,6 @@ class PreparedFrame:
         vtx_off += ctx.item_vtx_off
         idx_off = np.asarray([geo.idx_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
         idx_off += ctx.item_idx_off
-        ml_off = np.asarray([geo.ml_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
-        cb_off = np.asarray([geo.cb_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
         p = projection_vector(camera)
         p0, p1 = float(p[0]), float(p[1])
         self.p0, self.p1 = p0, p1
@@ -332,8 +330,6 @@ class PreparedFrame:
         k_mw = up.add(ctx.item_mw.reshape(-1))
         k_vo = up.add(vtx_off)
         k_io = up.add(idx_off)
-        k_mo = up.add(ml_off)
-        k_co = up.add(cb_off)
         k_lo = up.add(ilv_off)
         k_f = up.add(filt.reshape(-1))
         k_q = up.add(qgrid.reshape(-1).astype(np.float64))
@@ -371,14 +367,6 @@ class PreparedFrame:
         if ilv is not None:
             f.item_ilv_off = up.ptr(k_lo)
             f.indices_ilv = ilv.data_ptr()
-        if geo.chunk_box is not None:
-            f.item_cb_off = up.ptr(k_co)
-            f.chunk_box = geo.chunk_box.data_ptr()
-        if geo.ml_voff is not None:
-            f.item_ml_off = up.ptr(k_mo)
-            f.ml_voff = geo.ml_voff.data_ptr()
-            f.ml_verts = geo.ml_verts.data_ptr()
-            f.ml_tris = geo.ml_tris.data_ptr()
         f.instanced = int(self.inst_kernel)
         f.use_filter = int(self.use_filter)
         f.n_groups = len(ctx.group_item_count)
@@ -578,9 +566,7 @@ class PreparedFrame:
                                 tiles=int(s2[4]), fragments=int(s2[3]))
         st.stage3 = Stage3Stats(entries=int(c[N.C_Q3]), fragments=int(c[N.C_S3]))
         st.merge_s, st.stage1_s, st.stage2_s, st.stage3_s = secs
-        st.proved_fp32 = int(c[N.C_PROVED])
-        st.exact_fallbacks = (int(c[N.C_QX]) - int(c[N.C_QXHOLES]) + int(c[N.C_EXACT])
-                              - st.proved_fp32)
+        st.exact_fallbacks = int(c[N.C_QX]) - int(c[N.C_QXHOLES]) + int(c[N.C_EXACT])
         return st
 
 

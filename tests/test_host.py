@@ -242,38 +242,25 @@ def test_device_copy_cache_is_identity_checked():
     assert dv.device_mesh(m, cpu) is not b
 
 
-def test_build_meshlets_roundtrip_and_overflow():
-    """device.build_meshlets: every triangle's u8 local indices map back to its
-    vertex ids; meshlets with > CURAST_MESHLET_MAX_VERTS vertices are marked
-    by their count (the kernel then reads the index stream)."""
+def test_build_index_steps_lane_major_layout():
+    """device.build_index_steps (curast.h indices_ilv): per 128-triangle
+    step, lane l's 12 words are triangles l, l+32, l+64, l+96 (3 indices
+    each), zero past the mesh."""
     import torch
 
     from paper_2604_21749_b200 import device as dv
-    for T, scatter in ((1000, False), (777, True)):
-        rng = np.random.default_rng(T)
-        if scatter:
-            idx = rng.integers(0, 5000, size=3 * T).astype(np.uint32)
-        else:
-            idx = grid_indices(30)[:3 * T].astype(np.uint32)
-        voff, verts, tris = dv.build_meshlets(torch.from_numpy(idx.view(np.int32)), T)
-        voff, verts, tris = voff.numpy(), verts.numpy(), tris.numpy()
-        MT, MB = N.MESHLET_TRIS, N.MESHLET_BYTES
-        nm = -(-T // MT)
-        assert len(voff) == nm + 1 and len(tris) == nm * MB
-        for m in range(nm):
-            vl = verts[voff[m]:voff[m + 1]]
-            assert np.all(np.diff(vl.astype(np.int64)) > 0)      # ascending, unique
-            tt = np.arange(m * MT, min(T, m * MT + MT))
-            want = idx.reshape(-1, 3)[tt]
-            if len(vl) > N.MESHLET_MAX_VERTS:
-                assert scatter
-                continue
-            slot = tris[m * MB:m * MB + 3 * len(tt)].reshape(-1, 3).astype(np.int64)
-            loc = slot - slot // 17                              # inverse of j + j // 16
-            assert np.array_equal(loc + loc // 16, slot)
-            assert np.array_equal(vl[loc].astype(np.uint32), want)
-        if scatter:
-            assert (np.diff(voff) > N.MESHLET_MAX_VERTS).any()
+    for T in (1, 127, 128, 300):
+        idx = (np.arange(3 * T, dtype=np.uint32) * 7 + 1)
+        st = dv.build_index_steps(torch.from_numpy(idx.view(np.int32)), T).numpy().view(np.uint32)
+        ns = -(-T // 128)
+        assert st.size == ns * 384
+        w = st.reshape(ns, 32, 4, 3)
+        for s_ in range(ns):
+            for lane in range(32):
+                for k in range(4):
+                    t = s_ * 128 + lane + 32 * k
+                    want = idx[3 * t:3 * t + 3] if t < T else np.zeros(3, np.uint32)
+                    assert np.array_equal(w[s_, lane, k], want)
 
 
 def _grazing_transforms(rng, cam, n):

@@ -72,7 +72,7 @@ def measure(name, steps=20, check=False):
         "geometry_bytes_resident": geo_bytes,
         "pos_format": int(geo.pos_format), "idx_format": int(geo.idx_format),
         "stats": {"s1": vars(st.stage1), "s2": vars(st.stage2), "s3": vars(st.stage3),
-                  "exact_fallbacks": st.exact_fallbacks, "proved_fp32": st.proved_fp32},
+                  "exact_fallbacks": st.exact_fallbacks},
     }
     if check:
         from oracle import host as oh
