@@ -23,6 +23,23 @@
 
 namespace curast {
 
+// lean_load through volatile non-coherent loads (kept inside the step loop).
+__device__ __forceinline__ float4 ldg_step(const float *p) {
+    float4 v;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void lean_load_step(LeanConsts &F, const float *p) {
+    const float4 a = ldg_step(p), b = ldg_step(p + 4), c = ldg_step(p + 8), d = ldg_step(p + 12);
+    F.cx = make_float2(a.x, b.x);
+    F.cy = make_float2(a.y, b.y);
+    F.cz = make_float2(a.z, b.z);
+    F.c3 = make_float2(a.w, b.w);
+    F.dx = c.x; F.dy = c.y; F.dz = c.z; F.d3 = c.w;
+    F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
+}
+
 // One projected vertex (filter units): P = (X', Y') / d', D = d'.
 struct PV {
     float2 P;
@@ -137,23 +154,13 @@ __host__ __device__ constexpr int strip_g(int kind, int k) {
 static_assert(strip_r(1, 3) == 5 && strip_r(1, 5) == 11 && strip_r(2, 3) == 4 &&
               strip_r(2, 5) == 10, "strip refs");
 
-// The 4 decisions of a strip lane (6 distinct vertices, each gathered and
-// projected once, one lane bound): need bits in bits 0-3, frustum bits in
-// bits 4-7, bit 8 = the lane's vertices are provably in front of the near
-// plane and inside the viewport (CURAST_QX_INTERIOR for its queue entries).
+// Decisions of a strip lane's 4 triangles from its 6 distinct projected
+// vertices under one lane bound: need bits in bits 0-3, frustum bits in bits
+// 4-7, bit 8 = the lane's vertices are provably in front of the near plane
+// and inside the viewport (CURAST_QX_INTERIOR for its queue entries).
 template <int KIND>
-__device__ __forceinline__ unsigned lane_decide_strip(const LeanConsts &F,
-                                                      const float4 *__restrict__ pb,
-                                                      const uint32_t *ix, float W, float H,
-                                                      float slack, bool tiny) {
-    PV v[6];
-    {
-        float4 q[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) q[k] = __ldg(pb + ix[strip_r(KIND, k)]);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) v[k] = pv_project(F, q[k]);
-    }
+__device__ __forceinline__ unsigned strip_bits(const LeanConsts &F, const PV *v, float W, float H,
+                                               float slack, bool tiny) {
     const LaneB L = lane_bound<6>(F, v, W, H, slack);
     unsigned bits = L.interior ? 0x100u : 0u;
     if (__all_sync(0xffffffffu, L.interior)) {
@@ -165,8 +172,7 @@ __device__ __forceinline__ unsigned lane_decide_strip(const LeanConsts &F,
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const unsigned b = tri_full(v[strip_g(KIND, 3 * t)], v[strip_g(KIND, 3 * t + 1)],
-                                        v[strip_g(KIND, 3 * t + 2)], L, W, H,
-                                        tiny);
+                                        v[strip_g(KIND, 3 * t + 2)], L, W, H, tiny);
             bits |= ((b & 1u) << t) | ((b >> 1) << (4 + t));
         }
     }
@@ -176,10 +182,10 @@ __device__ __forceinline__ unsigned lane_decide_strip(const LeanConsts &F,
 // Generic lane (no strip pattern): triangle by triangle, 3 gathers and a
 // per-triangle bound each (lean_bits), so only one triangle's vertices are
 // live at a time.
-__device__ __forceinline__ unsigned lane_decide_generic(const LeanConsts &F,
-                                                        const float4 *__restrict__ pb,
-                                                        const uint32_t *ix, float W, float H,
-                                                        float slack, bool tiny) {
+__device__ __forceinline__ unsigned generic_bits(const LeanConsts &F,
+                                                 const float4 *__restrict__ pb,
+                                                 const uint32_t *ix, float W, float H,
+                                                 float slack, bool tiny) {
     unsigned bits = 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -192,12 +198,15 @@ __device__ __forceinline__ unsigned lane_decide_generic(const LeanConsts &F,
     return bits;
 }
 
-__device__ __forceinline__ unsigned lane_decide(int kind, const LeanConsts &F,
-                                                const float4 *__restrict__ pb, const uint32_t *ix,
-                                                float W, float H, float slack, bool tiny) {
-    if (kind == 1) return lane_decide_strip<1>(F, pb, ix, W, H, slack, tiny);
-    if (kind == 2) return lane_decide_strip<2>(F, pb, ix, W, H, slack, tiny);
-    return lane_decide_generic(F, pb, ix, W, H, slack, tiny);
+// One 48-byte fp64-queue entry: 9 positions + tag (CURAST_QX_WORDS).
+__device__ __forceinline__ void qx_put(const curast_frame_t &f, long long slot, const float3 &a,
+                                       const float3 &b, const float3 &c, long long tag) {
+    if (slot >= f.qx_cap) return;
+    int64_t *e = f.qx + CURAST_QX_WORDS * slot;
+    *(float4 *)e = make_float4(a.x, a.y, a.z, b.x);
+    *(float4 *)(e + 2) = make_float4(b.y, b.z, c.x, c.y);
+    *(float2 *)(e + 4) = make_float2(c.z, 0.0f);
+    e[CURAST_QX_TAG] = tag;
 }
 
 // The warp's 128-triangle step at chunk offset s0: indices of triangles
@@ -238,6 +247,64 @@ __device__ __forceinline__ bool claim_flat(const curast_frame_t &f, int lane, in
     return true;
 }
 
+// One warp step of k_s1_v2 for a lane pattern KIND (warp-uniform): gather,
+// decide, count, queue the undecided triangles with their positions.  The
+// strip kinds keep their 6 gathered positions for the queue entries.
+template <int KIND>
+__device__ __forceinline__ void v2_step(const curast_frame_t &f, const LeanConsts &F,
+                                        const float4 *__restrict__ pb, const uint32_t *ix, int nv,
+                                        long long tag, float W, float H, float slack, bool tiny,
+                                        unsigned &cnt16, QxReserve &R,
+                                        unsigned long long *qcount, int lane, unsigned lt_mask) {
+    float3 p[KIND == 0 ? 1 : 6];
+    unsigned bits;
+    if (KIND == 0) {
+        bits = generic_bits(F, pb, ix, W, H, slack, tiny);
+    } else {
+        PV v[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const float4 q = __ldg(pb + ix[strip_r(KIND, k)]);
+            p[k] = make_float3(q.x, q.y, q.z);
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] = pv_project(F, make_float4(p[k].x, p[k].y, p[k].z, 0.f));
+        bits = strip_bits<KIND>(F, v, W, H, slack, tiny);
+    }
+    const unsigned vmask = (1u << nv) - 1u;
+    const unsigned need = bits & vmask, fr = (bits >> 4) & vmask;
+    cnt16 += (unsigned)__popc(fr) + ((unsigned)(nv - __popc(need) - __popc(fr)) << 16);
+    unsigned b[4];
+    int tot = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        b[t] = __ballot_sync(0xffffffffu, (need >> t) & 1u);
+        tot += __popc(b[t]);
+    }
+    if (!tot) return;
+    const QxSlots qs = qx_reserve(R, qcount, tot, lane);
+    const long long flag = (bits & 0x100u) ? CURAST_QX_INTERIOR : 0ll;
+    int base = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        if ((need >> t) & 1u) {
+            const long long slot = qs.at(base + __popc(b[t] & lt_mask));
+            if (KIND == 0) {
+                // generic lanes re-read the positions (L1 hits) instead of
+                // keeping 12 gathered vertices live
+                const float4 va = __ldg(pb + ix[3 * t]), vb = __ldg(pb + ix[3 * t + 1]),
+                             vc = __ldg(pb + ix[3 * t + 2]);
+                qx_put(f, slot, make_float3(va.x, va.y, va.z), make_float3(vb.x, vb.y, vb.z),
+                       make_float3(vc.x, vc.y, vc.z), (tag + t) | flag);
+            } else {
+                qx_put(f, slot, p[strip_g(KIND, 3 * t)], p[strip_g(KIND, 3 * t + 1)],
+                       p[strip_g(KIND, 3 * t + 2)], (tag + t) | flag);
+            }
+        }
+        base += __popc(b[t]);
+    }
+}
+
 // ------------------------------------------------ filter -> global fp64 queue
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
@@ -263,54 +330,31 @@ __global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
             flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
             cnt16 = 0;
         }
-        LeanConsts F;
-        lean_load(F, f.item_filter + CURAST_FILTER_FLOATS * item);
+        const float *frow = f.item_filter + CURAST_FILTER_FLOATS * item;
         const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + item);
         const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + item) + 3 * lo;
         const int n = (int)(hi - lo);
         const bool vec = (((uintptr_t)ib) & 15) == 0;
         const long long tag = (item << 40) | lo;
         for (int s0 = 0; s0 < n; s0 += STEP) {
+            // the filter block is re-read per step (L1 hits, not hoisted):
+            // its 15 registers are then not live across the whole loop
+            LeanConsts F;
+            lean_load_step(F, frow);
             const int o = s0 + 4 * lane;
             const int nv = max(0, min(4, n - o));
             uint32_t ix[12];
             load_step_indices(ib, o, nv, vec, ix);
             const int kind = strip_kind(ix, nv == 4);
-            const unsigned bits = lane_decide(kind, F, pb, ix, W, H, slack, tiny);
-            const unsigned vmask = (1u << nv) - 1u;
-            const unsigned need = bits & vmask, fr = (bits >> 4) & vmask;
-            cnt16 += (unsigned)__popc(fr) + ((unsigned)(nv - __popc(need) - __popc(fr)) << 16);
-            unsigned b[4];
-            int tot = 0;
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                b[t] = __ballot_sync(0xffffffffu, (need >> t) & 1u);
-                tot += __popc(b[t]);
-            }
-            if (tot) {
-                const QxSlots qs = qx_reserve(R, qcount, tot, lane);
-                int base = 0;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    if ((need >> t) & 1u) {
-                        const long long slot = qs.at(base + __popc(b[t] & lt_mask));
-                        if (slot < f.qx_cap) {
-                            int64_t *e = f.qx + CURAST_QX_WORDS * slot;
-                            // the entry's positions: re-read (L1 hits) for
-                            // the few queued triangles instead of keeping
-                            // every gathered vertex live
-                            const float4 va = __ldg(pb + ix[3 * t]), vb = __ldg(pb + ix[3 * t + 1]),
-                                         vc = __ldg(pb + ix[3 * t + 2]);
-                            *(float4 *)e = make_float4(va.x, va.y, va.z, vb.x);
-                            *(float4 *)(e + 2) = make_float4(vb.y, vb.z, vc.x, vc.y);
-                            *(float2 *)(e + 4) = make_float2(vc.z, 0.0f);
-                            e[CURAST_QX_TAG] =
-                                (tag + o + t) | ((bits & 0x100u) ? CURAST_QX_INTERIOR : 0ll);
-                        }
-                    }
-                    base += __popc(b[t]);
-                }
-            }
+            if (kind == 1)
+                v2_step<1>(f, F, pb, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
+                           lt_mask);
+            else if (kind == 2)
+                v2_step<2>(f, F, pb, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
+                           lt_mask);
+            else
+                v2_step<0>(f, F, pb, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
+                           lt_mask);
         }
     }
     qx_reserve_close(f, R, lane);
