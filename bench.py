@@ -2,20 +2,31 @@
 """Benchmark: CuRast 3-stage rasterizer on B200 — triangles/s and ms/frame at
 3840x2160 against the HBM roofline (BASELINE.json metric).
 
-Workload (N=1): BASELINE.json configs[1] = SURVEY §8(d) config B — the dense
-grid mesh in the reference's make_tessellated_quad layout, n=7071 ->
-99,998,082 pixel-sized triangles (50,013,184 vertices, positions rounded to
-float32), 3840x2160, camera framing the quad.  A step = one frame: VB clear +
-stages 1-3 (+ the ncclMin composite when N>1) over geometry resident in HBM.
-Inputs (1.8 GB of indices + positions) are far larger than the 126 MB L2.
+Workloads (``--mode``):
 
-N>1 (torchrun): weak scaling, sort-last — the scene holds N instances of the
-grid (one per rank, distinct global-ID ranges, side by side); every rank
-rasterizes its range into a full-resolution VB and the VBs are composited with
-an unsigned-min reduction over NCCL.
+* ``B`` (default).  N=1: BASELINE.json configs[1] = SURVEY §8(d) config B —
+  the dense grid mesh in the reference's make_tessellated_quad layout,
+  n=7071 -> 99,998,082 pixel-sized triangles (50,013,184 vertices, positions
+  rounded to float32), 3840x2160, camera framing the quad.  N>1 (torchrun):
+  weak scaling — N layers of that grid stacked 1e-3 apart in depth, each
+  covering the whole frame (N x 100M distinct global IDs); rank r rasterizes
+  layer r, so every rank's work is exactly config B; the VBs are composited
+  by unsigned min over NCCL.
+* ``strong``: config B's 100M triangles split over the N ranks
+  (shard_range of the global IDs).
+* ``E``: SURVEY §8(d) config E — distinct displaced n=1414 grids generated
+  in HBM (each rank materialises only its shard's meshes), sharded by
+  global-ID range; ``--e-meshes`` sets the scene size (default 4,750 meshes =
+  18.99B triangles at N >= 4, 1,188 meshes per GPU below that).
 
---impl reference: the reference's CPU path (C restatement of its numba
-kernels, oracle/, all host threads) on the same config; rank 0 only.
+A step = one frame: VB clear + stages 1-3 (one CUDA-graph replay) + the
+ncclReduceScatter(u64, min) composite when N>1, geometry resident in HBM
+(1.8 GB per rank >> 126 MB L2: no flush needed).
+
+--impl reference: the reference's own CPU path — trirast.render_draw_list
+(numba kernels, installed in baseline/_ref) with all host threads — on the
+same config; rank 0 only.  Without baseline/_ref it falls back to the C
+restatement of the same kernels (oracle/, kind "port").
 """
 
 from __future__ import annotations
@@ -32,9 +43,12 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 METRIC = "triangles/sec and ms/frame at 3840x2160 (1/2/4/8 B200) vs HBM roofline"
 UNIT = "triangles/s"
+LAYER_DZ = 1e-3           # weak-scaling layer spacing (object units)
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_stage1_traffic.json")
 
 
 def _peaks():
@@ -75,9 +89,6 @@ class ClockSampler:
         self.temps = {}
 
     def _thermals(self, tag):
-        # GPU / HBM temperature and board power around the timed region (the
-        # filter kernel is latency-bound; its run-to-run modes are compared
-        # against these in DESIGN.md)
         nv = self.nv
         try:
             self.temps[f"gpu_temp_c_{tag}"] = int(nv.nvmlDeviceGetTemperature(self.h, nv.NVML_TEMPERATURE_GPU))
@@ -120,22 +131,42 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples), **self.temps}
 
 
-def build_scene(world: int, rank: int, n: int):
+# ------------------------------------------------------------------ workloads
+def e_meshes_default(world: int) -> int:
+    return 4750 if world >= 4 else 1188 * world
+
+
+def build_workload(mode: str, world: int, n: int, e_meshes: int | None):
+    """(scene, camera, description, scaling) of a bench mode."""
     from paper_2604_21749_b200 import generators as gen
     from paper_2604_21749_b200.scene import SceneNode
+    if mode == "E":
+        m = e_meshes or e_meshes_default(world)
+        scene, cam = gen.config_e(n_meshes=m, on_device=True)
+        return scene, cam, (f"E: {m} distinct displaced n=1414 grids generated in HBM "
+                            f"(SURVEY §8(d)), sort-last over {world} GPU(s)"), "strong"
     scene, cam = gen.config_b(n=n)
-    if world > 1:
-        # N instances of the same grid, side by side in one row of the frame
+    desc = (f"B: dense grid n={n} (make_tessellated_quad layout) @3840x2160, f32 positions")
+    if mode == "B" and world > 1:
         mesh = scene[0].mesh
-        transforms = []
-        s = 1.0 / world
-        for r in range(world):
-            m = np.eye(4)
-            m[:3, :3] *= s
-            m[0, 3] = (r - (world - 1) / 2.0) * s
-            transforms.append(m)
-        scene = [SceneNode(mesh=mesh, transforms=transforms)]
-    return scene, cam
+        layers = []
+        for k in range(world):
+            T = np.eye(4)
+            T[2, 3] = -LAYER_DZ * k
+            layers.append(SceneNode(mesh=mesh, transforms=[T]))
+        return layers, cam, (desc + f"; weak scaling: {world} stacked layers, "
+                             "rank r rasterizes layer r"), "weak"
+    if mode == "strong":
+        return scene, cam, desc + f"; strong scaling over {world} GPU(s)", "strong"
+    return scene, cam, desc, "weak"
+
+
+def rank_range(mode: str, dl, world: int, rank: int):
+    from paper_2604_21749_b200.distributed import shard_range
+    if mode == "B" and world > 1:
+        p = dl.prefix_sums.astype(np.int64)
+        return int(p[rank]), int(p[rank + 1])
+    return shard_range(int(dl.total_triangles), world, rank)
 
 
 def run_ours(args):
@@ -143,9 +174,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2604_21749_b200 as cr
-    from paper_2604_21749_b200 import device as dv
-    from paper_2604_21749_b200.pipeline import PreparedFrame
     from paper_2604_21749_b200.distributed import Compositor
+    from paper_2604_21749_b200.pipeline import PreparedFrame
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -156,19 +186,16 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     t0 = time.time()
-    scene, cam = build_scene(world, rank, args.n)
+    scene, cam, desc, scaling = build_workload(args.mode, world, args.n, args.e_meshes)
     dl = cr.build_draw_list(scene, cam)
     cfg = cr.RasterConfig(instancing="off")
-    total = dl.total_triangles
-    per_rank = total // world
-    lo = rank * per_rank
-    hi = total if rank == world - 1 else lo + per_rank
-    mesh = scene[0].mesh
+    total = int(dl.total_triangles)
+    lo, hi = rank_range(args.mode, dl, world, rank)
     T_rank = hi - lo
-    V = mesh.vertex_count()
-    setup_s = time.time() - t0
 
     pf = PreparedFrame(dl, cam, cfg, work_range=(lo, hi), fresh_fb=False)
+    V_rank = int(sum(m.vertex_count for m in pf.geo.meshes))
+    setup_s = time.time() - t0
     comp = Compositor(pf.fb, world) if world > 1 else None
     c, _ = pf.run()                       # sizes the queues
     st = pf.stats(c, [0, 0, 0, 0])
@@ -184,7 +211,8 @@ def run_ours(args):
             # input: the finished VB exists once, spread over the ranks)
             comp.reduce_scatter_min(rank)
 
-    for _ in range(max(args.warmup, 3)):
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
         step()
     torch.cuda.synchronize()
     if world > 1:
@@ -202,7 +230,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     sampler.stop()
     ms = start.elapsed_time(end) / K
-    # per-stage split (same kernels, launch path with events between stages)
+    # per-stage split: the same kernels through the launch path with events
+    # between the stages, on the stream they are launched on
     K2 = min(K, 50)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K2)]
     for k in range(K2):
@@ -216,123 +245,226 @@ def run_ours(args):
         t = torch.tensor([ms, s1_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, s1_ms = float(t[0]), float(t[1])
-    # k_clear, k_s1_lean_flat, k_s1_exact, k_stage2, k_stage3 (+ the composite)
+    # k_clear, stage-1 filter, k_s1_exact, k_stage2, k_stage3 (+ the composite)
     launches_per_step = 5 + (0 if comp is None else comp.launches_per_call)
 
     # correctness guard on the benchmarked frame: stats are deterministic
     c2 = pf.read_counters()
     assert int(c2[2 + 7]) == st.stage1.fragments
 
+    e2e = None
+    if not args.profile:
+        e2e = e2e_measure(dl, cam, cfg, total, world, rank, steps=min(args.steps, 10),
+                          warmup=3)
     result = None
     if rank == 0:
         hbm, peak_kind = _peaks()
-        frac_v = T_rank / total if total else 1.0
-        s1_bytes = 12 * T_rank + 12 * V * frac_v
-        frame_bytes = 12 * total + 12 * V * (world if world > 1 else 1) + 8 * pf.width * pf.height
+        s1_bytes = 12 * T_rank + 12 * V_rank
+        W, H = pf.width, pf.height
         achieved = s1_bytes / (s1_ms * 1e-3) / 1e9
-        traffic = None
-        tf = os.path.join(ROOT, "profiles", "stage1_traffic.json")
-        if os.path.exists(tf):
+        traffic, traffic_src = None, None
+        if os.path.exists(TRAFFIC_FILE) and args.mode != "E":
             try:
-                traffic = json.load(open(tf)).get("bytes_per_launch")
+                tj = json.load(open(TRAFFIC_FILE))
+                traffic, traffic_src = tj.get("bytes_per_launch"), tj.get("source")
             except Exception:
-                traffic = None
+                pass
         result = {
             "metric": METRIC, "value": total / (ms * 1e-3), "unit": UNIT,
-            "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3),
+            "n_gpus": world, "steps": K, "warmup": warm,
             "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "B: dense grid n=7071 (make_tessellated_quad layout), "
-                                   f"{total} triangles @3840x2160, f32 positions",
-                       "triangles": total, "vertices_per_mesh": V,
-                       "width": pf.width, "height": pf.height,
+            "config": {"workload": desc, "mode": args.mode,
+                       "triangles": total, "triangles_per_rank": T_rank,
+                       "vertices_per_rank": V_rank, "width": W, "height": H,
                        "parallelism": f"sort-last x{world}" if world > 1 else "single",
-                       "composite": "ncclReduceScatter(u64, min) into row stripes" if world > 1 else None,
-                       "l2": "inputs 1.8 GB per GPU >> 126 MB L2 (no flush needed)",
-                       "stage1_variant": os.environ.get("CURAST_S1", "lean"),
+                       "composite": "ncclReduceScatter(u64, min) into row stripes"
+                       if world > 1 else None,
+                       "l2": "inputs >= 1.8 GB per GPU >> 126 MB L2 (no flush needed)",
+                       "stage1_kernels": "k_s1_v2 (fp32 cull filter) + k_s1_exact (fp64)",
                        "frame_launch": "one CUDA graph replay per frame (PreparedFrame.capture); "
                                        "stage_ms from the launch path with events between stages",
                        "stage_ms": {"clear": clr_ms, "stage1": s1_ms, "stage2": s2_ms,
                                     "stage3": s3_ms},
                        "exact_fp64_fraction": st.exact_fallbacks / max(1, T_rank),
-                       "frame_hbm_frac": frame_bytes / (ms * 1e-3) / 1e9 / hbm,
+                       "frame_hbm_frac": (s1_bytes + 8 * W * H) / (ms * 1e-3) / 1e9 / hbm,
                        "stats": {"rasterized": st.stage1.rasterized,
                                  "tiny": st.stage1.culled_tiny,
                                  "fragments": st.fragments},
                        "setup_s": setup_s},
-            "roofline": {"bound": "hbm", "kernel": "stage 1 = k_s1_lean_flat (fp32 cull) + k_s1_exact (fp64 classify+raster)",
+            "roofline": {"bound": "hbm",
+                         "kernel": "stage 1 = k_s1_v2 (fp32 cull) + k_s1_exact (fp64 classify+raster)",
                          "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / hbm,
                          "algorithmic_bytes_per_launch": s1_bytes,
-                         "traffic": traffic},
+                         "algorithmic_bytes": "12 B per triangle (u32 indices) + 12 B per vertex "
+                                              "(f32 xyz) of this rank's shard",
+                         "traffic": traffic, "traffic_source": traffic_src},
             "clocks": sampler.report(),
             "gpu_launches": launches_per_step * K,
         }
-        if not args.profile:
-            result["e2e"] = e2e_measure(dl, cam, cfg, total, world, steps=min(args.steps, 10),
-                                        warmup=max(3, args.warmup))
-            if world == 1 and not args.no_cpu_baseline:
-                result["cpu_baseline"] = cpu_baseline(scene, cam, dl, total)
+        if e2e is not None:
+            result["e2e"] = e2e
+        if world == 1 and not args.profile and not args.no_cpu_baseline and args.mode != "E":
+            result["cpu_baseline"] = cpu_baseline(args.n)
     if world > 1:
         dist.barrier()
+        from paper_2604_21749_b200.distributed import close_comms
+        close_comms()
         dist.destroy_process_group()
     return result
 
 
-def e2e_measure(dl, cam, cfg, total, world, steps=5, warmup=3):
-    """Through the public drop-in call: render_draw_list(dl, cam, cfg) then
-    Framebuffer.words (the reference's host np.uint64 array).  Per step: host
-    descriptor build + pinned H2D, stages 1-3, counters + VB D2H.  Geometry
-    stays resident (uploaded once, like the reference's per-mesh decode
-    cache, scenecore.py:150-166); the cold number includes its upload."""
+def e2e_measure(dl, cam, cfg, total, world, rank, steps=5, warmup=3):
+    """Through the public drop-in call: render_draw_list(dl, cam, cfg) (N>1:
+    distributed.render_sharded over all ranks) then Framebuffer.words, the
+    reference's host np.uint64 array.  Per step: per-frame descriptor H2D,
+    stages 1-3 (+ the composite), counters + VB D2H.  Geometry stays resident
+    (uploaded once, like the reference's per-mesh decode cache,
+    scenecore.py:150-166); the cold number includes its upload (N=1)."""
     import torch
+    import torch.distributed as dist
 
     import paper_2604_21749_b200 as cr
     from paper_2604_21749_b200 import device as dv
-    from paper_2604_21749_b200.pipeline import PreparedFrame
+    from paper_2604_21749_b200.distributed import render_sharded
+
+    def call():
+        if world > 1:
+            fb, _ = render_sharded(dl, cam, cfg)
+        else:
+            fb, _ = cr.render_draw_list(dl, cam, cfg)
+        return fb.words
+
     for _ in range(max(1, warmup)):
-        fb, st = cr.render_draw_list(dl, cam, cfg)
-        words = fb.words
+        words = call()
     reps = max(1, steps)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(reps):
-        fb, st = cr.render_draw_list(dl, cam, cfg)
-        words = fb.words
+        words = call()
     t = (time.perf_counter() - t0) / reps
-    pf = PreparedFrame(dl, cam, cfg)
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    from paper_2604_21749_b200.pipeline import _frame_cache
+    pf = next(reversed(_frame_cache.values()))
     h2d = pf.h2d_bytes
-    d2h = words.nbytes + 8 * 32
+    d2h = words.nbytes + 8 * 40
     out = {"value": total / t, "unit": UNIT, "ms_per_step": t * 1e3,
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-           "api": "paper_2604_21749_b200.render_draw_list + Framebuffer.words"}
-    # cold: geometry upload inside the timed region (fresh device caches)
-    mesh = dl.items[0].mesh
-    dv.drop_device_copies([mesh])
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    fb, st = cr.render_draw_list(dl, cam, cfg)
-    words = fb.words
-    tc = time.perf_counter() - t0
-    geo_bytes = sum(int(m.positions.numel() * m.positions.element_size()
-                        + m.indices.numel() * m.indices.element_size())
-                    for m in dv.scene_geometry([mesh], torch.device("cuda", torch.cuda.current_device())).meshes)
-    out["cold"] = {"value": total / tc, "ms_per_step": tc * 1e3,
-                   "h2d_bytes_per_step": int(h2d + geo_bytes),
-                   "d2h_bytes_per_step": int(d2h)}
+           "api": "paper_2604_21749_b200.render_draw_list + Framebuffer.words"
+           if world == 1 else "paper_2604_21749_b200.distributed.render_sharded + Framebuffer.words"}
+    if world == 1 and not hasattr(dl.items[0].mesh, "generate"):
+        # cold: geometry upload inside the timed region (fresh device caches)
+        meshes = list({id(it.mesh): it.mesh for it in dl.items}.values())
+        dv.drop_device_copies(meshes)
+        _frame_cache.clear()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        words = call()
+        tc = time.perf_counter() - t0
+        dev = torch.device("cuda", torch.cuda.current_device())
+        geo_bytes = sum(int(m.positions.numel() * m.positions.element_size()
+                            + m.indices.numel() * m.indices.element_size())
+                        for m in dv.scene_geometry(meshes, dev).meshes)
+        out["cold"] = {"value": total / tc, "ms_per_step": tc * 1e3,
+                       "h2d_bytes_per_step": int(h2d + geo_bytes),
+                       "d2h_bytes_per_step": int(d2h)}
     return out
 
 
-def cpu_baseline(scene, cam, dl, total, budget_s=20.0):
-    """The reference's CPU path (oracle/ C restatement of kernels.py, threaded
-    like pipeline.py) on this host's cores, on a bounded sample of config B."""
+# ------------------------------------------------------- the reference's CPU path
+def _trirast():
+    """The unmodified reference package (trirast, numba) from baseline/_ref,
+    or None when it is not installed."""
+    if not os.path.isdir(os.path.join(REF_PATH, "trirast")):
+        return None
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    try:
+        import trirast
+        import trirast.pipeline  # noqa: F401
+        return trirast
+    except Exception:
+        return None
+
+
+class RefFrame:
+    """Config B (or its first ``sample`` triangles: whole grid rows in
+    global-ID order, the same vertices) in the reference's own types, with
+    its draw list and RenderContext built once (the reference's per-call
+    host setup, pipeline.py:217-218, is not part of its kernel time)."""
+
+    def __init__(self, tr, n: int, sample: int | None = None):
+        from paper_2604_21749_b200 import generators as gen
+        scene, cam = gen.config_b(n=n)
+        m = scene[0].mesh
+        idx = m.indices if sample is None else m.indices[:3 * sample]
+        self.mesh = tr.Mesh(positions=m.positions, indices=np.ascontiguousarray(idx),
+                            triangle_count=len(idx) // 3, aabb=m.aabb)
+        self.cam = tr.Camera(position=cam.position, view_transform=cam.view_transform,
+                             fovy=cam.fovy, aspect=cam.aspect, near=cam.near,
+                             image_width=cam.image_width, image_height=cam.image_height)
+        self.dl = tr.build_draw_list([tr.SceneNode(mesh=self.mesh, transforms=[np.eye(4)])],
+                                     self.cam)
+        self.ctx = tr.pipeline.build_context(self.dl, self.cam)
+        self.tr = tr
+        self.total = int(self.dl.total_triangles)
+
+    def render(self, workers: int, batch: int) -> float:
+        cfg = self.tr.RasterConfig(workers=workers, batch_size=batch,
+                                   stage2_capacity=1 << 20, stage3_capacity=1 << 20)
+        t0 = time.perf_counter()
+        self.tr.render_draw_list(self.dl, self.cam, cfg, ctx=self.ctx)
+        return time.perf_counter() - t0
+
+
+def _ref_sample(tr, n: int, cores: int, seconds: float) -> int:
+    """Triangles of config B the reference renders in about ``seconds`` on
+    ``cores`` threads (rate from a 1/50 probe, JIT compiled first)."""
+    total = 2 * n * n
+    probe = RefFrame(tr, n, max(4096, total // 50))
+    probe.render(cores, 4096)                       # numba compile / load cache
+    dt = min(probe.render(cores, 4096) for _ in range(2))
+    rate = probe.total / max(dt, 1e-9)
+    return int(min(total, max(probe.total, rate * seconds)))
+
+
+def cpu_baseline(n: int, budget_s: float = 12.0):
+    """cpu_baseline of the GPU arm: the reference's own render_draw_list
+    (numba, all host threads, batch 4096) on a bounded sample of config B."""
+    cores = len(os.sched_getaffinity(0))
+    tr = _trirast()
+    if tr is None:
+        return cpu_baseline_port(n, budget_s)
+    total = 2 * n * n
+    sample = _ref_sample(tr, n, cores, budget_s)
+    fr = RefFrame(tr, n, sample)
+    fr.render(cores, 4096)
+    dt = fr.render(cores, 4096)
+    return {"value": sample / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"first {sample} global IDs of config B ({sample / total:.1%} of the "
+                      f"frame: whole grid rows, same vertices) through trirast.render_draw_list "
+                      f"(baseline/_ref, numba 0.65), workers={cores}, batch 4096",
+            "seconds": dt}
+
+
+def cpu_baseline_port(n: int, budget_s: float = 12.0):
+    """Fallback without baseline/_ref: the C restatement of the reference's
+    kernels (oracle/), threaded like pipeline.py, on a bounded sample."""
     from oracle import host as oh
+    from paper_2604_21749_b200 import generators as gen
+    scene, cam = gen.config_b(n=n)
     cores = len(os.sched_getaffinity(0))
     odl = oh.build_draw_list(scene, cam)
     ctx = oh.build_context(odl, cam)
     cc = oh.camera_constants(cam)
-    # calibrate on a 1/50 slice, then size the sample to ~budget_s/2
+    total = odl.total
     probe = max(1, total // 50)
     _, _, rc, _, dt = oh.render_context(ctx, cc, workers=cores, batch=4096,
                                         work_range=(0, probe), s2_cap=1 << 20, s3_cap=1 << 20)
@@ -348,25 +480,68 @@ def cpu_baseline(scene, cam, dl, total, budget_s=20.0):
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU implementation of the path on the
-    host cores (oracle port; rank 0 only)."""
+    """--impl reference: trirast.render_draw_list (the reference's numba CPU
+    path from baseline/_ref) with all host threads on config B, each step a
+    bounded sample (whole grid rows) so the run ends within a few minutes;
+    rank 0 only.  Also reports the worker / batch rows of BASELINE.md §2 on a
+    smaller sample."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
+    tr = _trirast()
+    if tr is None:
+        return run_reference_port(args)
+    cores = len(os.sched_getaffinity(0))
+    n = args.n
+    total = 2 * n * n
+    steps, warm = args.steps, max(args.warmup, 1)
+    per_step = 150.0 / (steps + warm)
+    sample = _ref_sample(tr, n, cores, per_step)
+    fr = RefFrame(tr, n, sample)
+    times = []
+    for k in range(steps + warm):
+        dt = fr.render(cores, 4096)
+        if k >= warm:
+            times.append(dt)
+    ms = float(np.mean(times)) * 1e3
+    value = sample / (ms * 1e-3)
+    # BASELINE.md §2 rows: 1 / all workers x batch 256 / 4096 on ~2M triangles
+    rows = {}
+    small = RefFrame(tr, n, min(sample, 2_000_000))
+    for w in (1, cores):
+        for b in (256, 4096):
+            small.render(w, b)
+            rows[f"workers={w},batch={b}"] = small.total / small.render(w, b)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps, "warmup": warm,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"B: dense grid n={n} (make_tessellated_quad layout) @3840x2160, "
+                               "f32 positions",
+                   "triangles": total, "sample_triangles_per_step": sample,
+                   "rows_triangles_per_s": rows, "rows_sample_triangles": small.total},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"first {sample} global IDs of config B per step "
+                                   f"({sample / total:.1%} of a frame: whole grid rows) through "
+                                   f"trirast.render_draw_list (numba), workers={cores}, "
+                                   "batch 4096"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def run_reference_port(args):
+    """Fallback reference arm (no baseline/_ref): the oracle port."""
     from oracle import host as oh
-    scene, cam = build_scene(1, 0, args.n)
+    from paper_2604_21749_b200 import generators as gen
+    scene, cam = gen.config_b(n=args.n)
     odl = oh.build_draw_list(scene, cam)
     ctx = oh.build_context(odl, cam)
     cc = oh.camera_constants(cam)
     total = odl.total
     cores = len(os.sched_getaffinity(0))
-    steps = args.steps
-    warm = max(args.warmup, 1)
-    budget = 150.0                      # whole run within a few minutes
-    # the oracle call has a fixed cost (~0.4 s: per-worker frame buffers and
-    # their merge) besides its per-triangle work: two probes separate them, and
-    # a step is never smaller than a quarter of the frame, so the fixed cost
-    # does not dominate the reported rate when K is large
+    steps, warm = args.steps, max(args.warmup, 1)
     dts = []
     probes = (max(1, total // 50), max(2, total // 10))
     for n in probes:
@@ -374,7 +549,7 @@ def run_reference(args):
                                      s2_cap=1 << 20, s3_cap=1 << 20)[4])
     rate = (probes[1] - probes[0]) / max(dts[1] - dts[0], 1e-9)
     fixed = max(0.0, dts[0] - probes[0] / rate)
-    per_step = budget / (steps + warm)
+    per_step = 150.0 / (steps + warm)
     sample = int(min(total, max(total // 4, rate * max(per_step - fixed, 0.0))))
     times = []
     for k in range(steps + warm):
@@ -407,7 +582,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="B", choices=["B", "strong", "E"])
     ap.add_argument("--n", type=int, default=7071, help="grid tessellation (config B: 7071)")
+    ap.add_argument("--e-meshes", type=int, default=None, help="config E meshes (mode E)")
     ap.add_argument("--profile", action="store_true", help="skip e2e / CPU legs (ncu runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

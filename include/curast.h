@@ -198,6 +198,13 @@ int curast_min_u64(uint64_t *dst, const uint64_t *src, int64_t n, void *stream);
  * values.  Writes {checked, violations, max ratio*1e6} into out3 (device). */
 int curast_filter_check(const curast_frame_t *frame, int64_t *out3, void *stream);
 
+/* Diagnostics: the shared-reciprocal division of the fp64 pass
+ * (exact.cuh div_recip / div_shared) against IEEE __ddiv_rn / __drcp_rn on
+ * n hashed operand pairs (mode 0 random finite, 1 rasterizer magnitudes,
+ * 2 edge values).  Adds {checked, quotient mismatches, fallbacks to
+ * __ddiv_rn, reciprocal mismatches} into out4 (device int64[4]). */
+int curast_div_check(int64_t n, uint64_t seed, int32_t mode, int64_t *out4, void *stream);
+
 /* ---- resolve / shading (resolvepass.py:297-407) ---- */
 typedef struct curast_resolve {
     const uint64_t *fb;               /* visibility words                      */

@@ -117,6 +117,8 @@ def lib():
         fn.argtypes = [ctypes.POINTER(CurastFrame), _P]
     L.curast_filter_check.restype = _I32
     L.curast_filter_check.argtypes = [ctypes.POINTER(CurastFrame), _P, _P]
+    L.curast_div_check.restype = _I32
+    L.curast_div_check.argtypes = [_I64, ctypes.c_uint64, _I32, _P, _P]
     L.curast_fill_u64.restype = _I32
     L.curast_fill_u64.argtypes = [_P, _I64, ctypes.c_uint64, _P]
     L.curast_min_u64.restype = _I32
@@ -137,6 +139,7 @@ EXPORTED_SYMBOLS = (
     "curast_abi_version", "curast_last_error", "curast_chunk_tris",
     "curast_frame_clear", "curast_stage1", "curast_stage2", "curast_stage3",
     "curast_render", "curast_fill_u64", "curast_min_u64", "curast_filter_check",
+    "curast_div_check",
     "curast_resolve", "curast_downsample", "curast_debug_view",
 )
 

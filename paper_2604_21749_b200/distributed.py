@@ -225,17 +225,13 @@ def render_sharded(draw_list, camera, cfg=None, *, group=None):
     them for totals).  Only the meshes of this rank's shard are uploaded
     (``PreparedFrame(work_range=...)``)."""
     from .config import RasterConfig
-    from .pipeline import PreparedFrame, build_context
+    from .pipeline import _cached_frame, work_space
     from .scene import Framebuffer
     cfg = cfg or RasterConfig()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    ctx = build_context(draw_list, camera)
-    instanced = (cfg.instancing == "on"
-                 or (cfg.instancing == "auto" and ctx.max_instances >= 2))
-    space = int(ctx.group_prefix[-1]) if instanced else int(draw_list.total_triangles)
-    lo, hi = shard_range(space, world, rank)
-    pf = PreparedFrame(draw_list, camera, cfg, ctx, work_range=(lo, hi))
+    lo, hi = shard_range(work_space(draw_list, cfg), world, rank)
+    pf = _cached_frame(draw_list, camera, cfg, None, None, (lo, hi))
     c, secs = pf.run()
     st = pf.stats(c, secs)
     if world > 1:

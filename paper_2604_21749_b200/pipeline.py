@@ -153,6 +153,25 @@ def adopt_context(ctx, draw_list: DrawList, camera) -> RenderContext:
     return own
 
 
+def work_space(draw_list: DrawList, cfg: RasterConfig) -> int:
+    """Size of a frame's stage-1 work space: the unique triangles of the
+    instancing groups for an instanced frame (pipeline.py:244), else the
+    global triangle IDs.  Shards are ranges of this space."""
+    n = len(draw_list.items)
+    inst = cfg.instancing == "on"
+    if cfg.instancing == "auto" and n >= 2:
+        nodes = [it.node_index for it in draw_list.items]
+        inst = any(a == b for a, b in zip(nodes, nodes[1:]))   # a node with >= 2 instances
+    if not inst:
+        return int(draw_list.total_triangles)
+    tot, prev = 0, None
+    for it in draw_list.items:
+        if it.node_index != prev:
+            tot += int(it.triangle_count)
+            prev = it.node_index
+    return tot
+
+
 def shard_items(ctx: RenderContext, work_range, inst_kernel: bool) -> np.ndarray:
     """Boolean mask of the draw items a work range touches: the items whose
     global-ID range intersects it (flat work space), or every item of the

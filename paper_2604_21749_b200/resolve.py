@@ -96,13 +96,126 @@ def _attributes(meshes, geo, device):
     return a
 
 
+class _DeviceResolveStats(ResolveStats):
+    """ResolveStats whose counters stay on the device until first read, so
+    resolve_frame_device does not synchronise the host."""
+
+    def __init__(self, counters):
+        object.__setattr__(self, "_c", counters)
+        object.__setattr__(self, "_v", None)
+
+    def _vals(self):
+        if self._v is None:
+            object.__setattr__(self, "_v", [int(x) for x in self._c.cpu().tolist()[:3]])
+        return self._v
+
+    shaded = property(lambda self: self._vals()[0])
+    background = property(lambda self: self._vals()[1])
+    degenerate = property(lambda self: self._vals()[2])
+
+    def __repr__(self):
+        return (f"ResolveStats(shaded={self.shaded}, background={self.background}, "
+                f"degenerate={self.degenerate})")
+
+
+class PreparedResolve:
+    """The resolve descriptors of one (draw list, camera, shading) resident on
+    the device: built and uploaded once, reused by every resolve of frames
+    of that draw list (the per-call work is one kernel launch)."""
+
+    def __init__(self, draw_list, camera, shading, device):
+        ctx = build_context(draw_list, camera)
+        geo = scene_geometry(ctx.meshes, device)
+        attrs = _attributes(ctx.meshes, geo, device)
+        self.draw_list, self.geo, self.attrs = draw_list, geo, attrs
+        n = len(draw_list.items)
+        modes = np.asarray([_item_mode(ctx.meshes[i], shading.mode) for i in ctx.item_mesh],
+                           dtype=np.int32)
+        up = PackedUpload()
+        kp = up.add(ctx.prefix)
+        kmw = up.add(ctx.item_mw.reshape(-1))
+        kvo = up.add(np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64))
+        kio = up.add(np.asarray([geo.idx_off[i] for i in ctx.item_mesh], dtype=np.int64))
+        kq = up.add(np.stack([geo.meshes[i].qgrid for i in ctx.item_mesh]).reshape(-1))
+        kpk = up.add(np.asarray([geo.meshes[i].pack for i in ctx.item_mesh],
+                                dtype=np.int64).reshape(-1))
+        kmo = up.add(modes)
+        kco = up.add(np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64))
+        ktx = up.add(np.asarray([attrs.mesh_tex[i] for i in ctx.item_mesh], dtype=np.int64))
+        up.upload(device)
+        self.upload = up
+        r = N.CurastResolve()
+        r.n_items = n
+        r.prefix, r.item_mw = up.ptr(kp), up.ptr(kmw)
+        r.item_vtx_off, r.item_idx_off = up.ptr(kvo), up.ptr(kio)
+        r.pos_format, r.idx_format = geo.pos_format, geo.idx_format
+        r.positions, r.indices = geo.positions.data_ptr(), geo.indices.data_ptr()
+        r.item_qgrid, r.item_pack = up.ptr(kq), up.ptr(kpk)
+        r.item_mode, r.item_color_off = up.ptr(kmo), up.ptr(kco)
+        r.colors, r.uvs = attrs.colors.data_ptr(), attrs.uvs.data_ptr()
+        r.item_tex, r.tex_desc = up.ptr(ktx), attrs.tex_desc.data_ptr()
+        r.level_desc, r.texels = attrs.level_desc.data_ptr(), attrs.texels.data_ptr()
+        r.trilinear = int(shading.mip_filter == "trilinear")
+        r.headlight = int(bool(shading.headlight))
+        for i in range(4):
+            r.background[i] = int(shading.background[i])
+            r.base_color[i] = int(shading.base_color[i])
+        p = projection_vector(camera)
+        r.p0, r.p1 = float(p[0]), float(p[1])
+        pos = np.asarray(camera.position, dtype=np.float64)
+        rot = np.asarray(camera.view_transform, dtype=np.float64)[:3, :3].reshape(-1)
+        for i in range(3):
+            r.cam[i] = float(pos[i])
+        for i in range(9):
+            r.rot[i] = float(rot[i])
+        self.r = r
+        self.meshes = ctx.meshes
+
+    def current(self, device) -> bool:
+        return scene_geometry(self.meshes, device) is self.geo
+
+    def launch(self, words, w, h, out, counters, row0, nrows, stream=None):
+        r = self.r
+        r.fb = words.data_ptr()
+        r.width, r.height = w, h
+        r.out_rgba = out.data_ptr()
+        r.counters = counters.data_ptr()
+        r.row0, r.rows = row0, nrows
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        N.check(N.lib().curast_resolve(ctypes.byref(r), st), "resolve")
+
+
+_resolve_cache: dict = {}
+
+
+def _shading_key(s):
+    return (s.mode, tuple(s.background), tuple(s.base_color), s.mip_filter, bool(s.headlight))
+
+
+def prepared_resolve(draw_list, camera, shading, device) -> PreparedResolve:
+    """Cached PreparedResolve (by draw-list identity, camera and shading
+    values; at most 4 kept; rebuilt when the scene geometry changed)."""
+    from .pipeline import _camera_key
+    key = (id(draw_list), _camera_key(camera), _shading_key(shading), str(device))
+    pr = _resolve_cache.get(key)
+    if pr is not None and pr.draw_list is draw_list and pr.current(device):
+        return pr
+    if len(_resolve_cache) >= 4:
+        _resolve_cache.pop(next(iter(_resolve_cache)))
+    pr = PreparedResolve(draw_list, camera, shading, device)
+    _resolve_cache[key] = pr
+    return pr
+
+
 def resolve_frame_device(framebuffer, draw_list, camera, shading: ShadingConfig | None = None,
                          *, rows=None, stripe_words=None):
     """Shade every pixel on the GPU; returns (uint8 CUDA tensor [h, w, 4],
     ResolveStats).  ``rows=(row0, n)`` shades image rows [row0, row0 + n)
     only (a sort-last stripe) from ``stripe_words`` (int64 CUDA tensor of
-    n*w words; default: the framebuffer's rows) into an [n, w, 4] image."""
-    L = N.lib()
+    n*w words; default: the framebuffer's rows) into an [n, w, 4] image.
+    Nothing synchronises the host: the stats read their device counters on
+    first access; the descriptors are prepared once per draw list / camera /
+    shading (prepared_resolve)."""
     shading = shading or ShadingConfig()
     device = torch.device("cuda", torch.cuda.current_device())
     w, h = framebuffer.width, framebuffer.height
@@ -115,62 +228,13 @@ def resolve_frame_device(framebuffer, draw_list, camera, shading: ShadingConfig 
     if stripe_words is None and rows is not None:
         words = words[row0 * w:(row0 + nrows) * w]
     out = torch.empty((nrows, w, 4), dtype=torch.uint8, device=device)
-    counters = torch.zeros(4, dtype=torch.int64, device=device)
-    st = ResolveStats()
     if draw_list.total_triangles == 0 or len(draw_list.items) == 0:
         out[:] = torch.tensor(shading.background, dtype=torch.uint8, device=device)
-        st.background = w * nrows
-        return out, st
-    ctx = build_context(draw_list, camera)
-    geo = scene_geometry(ctx.meshes, device)
-    attrs = _attributes(ctx.meshes, geo, device)
-    n = len(draw_list.items)
-    modes = np.asarray([_item_mode(ctx.meshes[i], shading.mode) for i in ctx.item_mesh],
-                       dtype=np.int32)
-    up = PackedUpload()
-    kp = up.add(ctx.prefix)
-    kmw = up.add(ctx.item_mw.reshape(-1))
-    kvo = up.add(np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64))
-    kio = up.add(np.asarray([geo.idx_off[i] for i in ctx.item_mesh], dtype=np.int64))
-    kq = up.add(np.stack([geo.meshes[i].qgrid for i in ctx.item_mesh]).reshape(-1))
-    kpk = up.add(np.asarray([geo.meshes[i].pack for i in ctx.item_mesh], dtype=np.int64).reshape(-1))
-    kmo = up.add(modes)
-    kco = up.add(np.asarray([geo.vtx_off[i] for i in ctx.item_mesh], dtype=np.int64))
-    ktx = up.add(np.asarray([attrs.mesh_tex[i] for i in ctx.item_mesh], dtype=np.int64))
-    up.upload(device)
-    r = N.CurastResolve()
-    r.fb = words.data_ptr()
-    r.width, r.height, r.n_items = w, h, n
-    r.prefix, r.item_mw = up.ptr(kp), up.ptr(kmw)
-    r.item_vtx_off, r.item_idx_off = up.ptr(kvo), up.ptr(kio)
-    r.pos_format, r.idx_format = geo.pos_format, geo.idx_format
-    r.positions, r.indices = geo.positions.data_ptr(), geo.indices.data_ptr()
-    r.item_qgrid, r.item_pack = up.ptr(kq), up.ptr(kpk)
-    r.item_mode, r.item_color_off = up.ptr(kmo), up.ptr(kco)
-    r.colors, r.uvs = attrs.colors.data_ptr(), attrs.uvs.data_ptr()
-    r.item_tex, r.tex_desc = up.ptr(ktx), attrs.tex_desc.data_ptr()
-    r.level_desc, r.texels = attrs.level_desc.data_ptr(), attrs.texels.data_ptr()
-    r.trilinear = int(shading.mip_filter == "trilinear")
-    r.headlight = int(bool(shading.headlight))
-    for i in range(4):
-        r.background[i] = int(shading.background[i])
-        r.base_color[i] = int(shading.base_color[i])
-    p = projection_vector(camera)
-    r.p0, r.p1 = float(p[0]), float(p[1])
-    pos = np.asarray(camera.position, dtype=np.float64)
-    rot = np.asarray(camera.view_transform, dtype=np.float64)[:3, :3].reshape(-1)
-    for i in range(3):
-        r.cam[i] = float(pos[i])
-    for i in range(9):
-        r.rot[i] = float(rot[i])
-    r.out_rgba = out.data_ptr()
-    r.counters = counters.data_ptr()
-    r.row0, r.rows = row0, nrows
-    N.check(L.curast_resolve(ctypes.byref(r), torch.cuda.current_stream().cuda_stream),
-            "resolve")
-    c = counters.cpu().numpy()
-    st.shaded, st.background, st.degenerate = int(c[0]), int(c[1]), int(c[2])
-    return out, st
+        return out, ResolveStats(background=w * nrows)
+    counters = torch.zeros(4, dtype=torch.int64, device=device)
+    pr = prepared_resolve(draw_list, camera, shading, device)
+    pr.launch(words, w, h, out, counters, row0, nrows)
+    return out, _DeviceResolveStats(counters)
 
 
 def resolve_frame(framebuffer, draw_list, camera, shading: ShadingConfig | None = None):

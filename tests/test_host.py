@@ -386,3 +386,29 @@ def test_shard_items_select_only_the_ranks_geometry():
     assert len(np.unique(ctx.item_mesh[m0])) == 1
     m1 = shard_items(ctx, (g0, int(ctx.group_prefix[-1])), True)
     assert not (m0 & m1).any() and (m0 | m1).all()
+
+
+def test_benchcli_rows_mirror_the_reference_toggles(tmp_path):
+    """benchcli.bench_rows = cli.py:115-141: labels, configs, timing-only."""
+    from paper_2604_21749_b200 import benchcli
+    cam = Camera.look_at((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), width=64, height=48)
+    cfg = RasterConfig()
+    assert [r[0] for r in benchcli.bench_rows(cam, cfg)] == ["base"]
+    rows = benchcli.bench_rows(cam, cfg, "tinyCull")
+    assert [(r[0], r[2].tiny_cull, r[3]) for r in rows] == [("tinyCull=on", True, True),
+                                                          ("tinyCull=off", False, True)]
+    rows = benchcli.bench_rows(cam, cfg, "workers")
+    assert [r[2].workers for r in rows] == [1, 2, 4, 8] and all(r[3] for r in rows)
+    rows = benchcli.bench_rows(cam, cfg, "instancing")
+    assert [r[2].instancing for r in rows] == ["on", "off"]
+    rows = benchcli.bench_rows(cam, cfg, "superSampling")
+    assert [(r[1].supersampling, r[1].internal_width, r[3]) for r in rows] == [
+        (1, 64, False), (2, 128, False), (4, 256, False)]
+    with pytest.raises(ValueError):
+        benchcli.bench_rows(cam, cfg, "nope")
+    rep = [{c: (1.5 if c.endswith("Ms") else (3 if c in ("visibleTriangles", "fragments", "culled")
+                                               else "x")) for c in benchcli.COLS}]
+    out = tmp_path / "rows.csv"
+    benchcli.write_csv(rep, out)
+    assert out.read_text().splitlines()[0] == ",".join(benchcli.COLS)
+    assert "stage1Ms" in benchcli.format_table(rep).splitlines()[0]
