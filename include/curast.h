@@ -92,8 +92,7 @@ enum curast_error {
  * triangle's vertices in front of the near plane and inside the viewport
  * (k_s1_exact then skips those tests); items < 2^22 */
 #define CURAST_QX_INTERIOR (1ll << 62)
-/* triangles per stage-1 warp step (32 lanes x 4) and per lane-major index
- * step (indices_ilv) */
+/* triangles per stage-1 warp step (32 lanes x 4) */
 #define CURAST_STEP_TRIS 128
 
 /* fp64 work-queue entry: 6 int64 words (48 B) */
@@ -115,15 +114,6 @@ typedef struct curast_frame {
     const float *item_filter;         /* float[n_items][16] or NULL           */
     const double *item_qgrid;         /* U16: double[n_items][6] gmin, gsize  */
     const int64_t *item_pack;         /* PACKED: int64[n_items][2] min, bits  */
-    /* ---- lane-major index steps (POS_F32 + IDX_U32; optional) ----
-     * the u32 stream re-laid out per step of CURAST_STEP_TRIS triangles:
-     * 384 words, lane l's 12 words = triangles l, l+32, l+64, l+96 of the
-     * step (3 indices each, zero padded past the mesh).  One 3 x 128-bit
-     * load per lane, and each vertex gather of the warp then reads 32
-     * consecutive triangles' vertices (fewer L1 lines than 4 consecutive
-     * triangles per lane).                                                  */
-    const int64_t *item_ilv_off;      /* word offset of the item's mesh       */
-    const uint32_t *indices_ilv;
     /* ---- instancing groups (pipeline.py:114-135) ---- */
     int32_t instanced;                /* 1: stage1_instanced_range semantics  */
     int32_t use_filter;               /* 1: fp32 cull filter + fp64 fallback  */
@@ -181,8 +171,13 @@ typedef struct curast_frame {
 
 int curast_abi_version(void);
 const char *curast_last_error(void);
-/* triangles per stage-1 chunk the host work table must use for a variant */
+/* Stage-1 work chunks: the host work tables split their ranges in chunks of
+ * frame->chunk_tris (flat) / frame->inst_chunk_tris (instanced) triangles,
+ * each a multiple of curast_chunk_quantum() (128) and at most
+ * curast_chunk_tris(instanced) (2048): large chunks for streamed frames,
+ * small ones so that small frames still occupy every SM. */
 int64_t curast_chunk_tris(int32_t instanced);
+int64_t curast_chunk_quantum(void);
 
 int curast_frame_clear(const curast_frame_t *frame, void *stream);
 int curast_stage1(const curast_frame_t *frame, void *stream);

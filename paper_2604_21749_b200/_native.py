@@ -43,7 +43,6 @@ class CurastFrame(ctypes.Structure):
         ("n_items", _I64), ("prefix", _P), ("item_mv", _P), ("item_mw", _P),
         ("item_vtx_off", _P), ("item_idx_off", _P), ("item_filter", _P),
         ("item_qgrid", _P), ("item_pack", _P),
-        ("item_ilv_off", _P), ("indices_ilv", _P),
         ("instanced", _I32), ("use_filter", _I32),
         ("n_groups", _I64), ("group_prefix", _P), ("group_item_off", _P),
         ("group_item_count", _P), ("group_items", _P),
@@ -110,6 +109,8 @@ def lib():
     L.curast_last_error.restype = ctypes.c_char_p
     L.curast_chunk_tris.restype = _I64
     L.curast_chunk_tris.argtypes = [_I32]
+    L.curast_chunk_quantum.restype = _I64
+    L.curast_chunk_quantum.argtypes = []
     for name in ("curast_frame_clear", "curast_stage1", "curast_stage2",
                  "curast_stage3", "curast_render"):
         fn = getattr(L, name)
@@ -136,7 +137,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = (
-    "curast_abi_version", "curast_last_error", "curast_chunk_tris",
+    "curast_abi_version", "curast_last_error", "curast_chunk_tris", "curast_chunk_quantum",
     "curast_frame_clear", "curast_stage1", "curast_stage2", "curast_stage3",
     "curast_render", "curast_fill_u64", "curast_min_u64", "curast_filter_check",
     "curast_div_check",

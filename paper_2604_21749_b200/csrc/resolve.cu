@@ -93,8 +93,17 @@ __device__ __forceinline__ V3 pixel_dir(const curast_resolve_t &r, double xs, do
               a * R[2] + b * R[5] + c * R[8]);
 }
 
+__device__ __forceinline__ uint32_t rgba(uint32_t r, uint32_t g, uint32_t b, uint32_t a) {
+    return r | (g << 8) | (b << 16) | (a << 24);
+}
+
+// 4 resident blocks per SM (64 registers; 128 without the bound held
+// the kernel at 16 warps per SM, latency-bound on its gathers)
+#ifndef CURAST_RESOLVE_MINB
+#define CURAST_RESOLVE_MINB 4
+#endif
 template <int PF, int IF>
-__global__ void k_resolve(const curast_resolve_t r) {
+__global__ void __launch_bounds__(256, CURAST_RESOLVE_MINB) k_resolve(const curast_resolve_t r) {
     __shared__ unsigned long long s_cnt[3];
     if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -104,10 +113,10 @@ __global__ void k_resolve(const curast_resolve_t r) {
     for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < npix;
          pix += (int64_t)gridDim.x * blockDim.x) {
         uint64_t word = r.fb[pix];
-        uint8_t *o = r.out_rgba + 4 * pix;
+        // one 32-bit store per pixel (RGBA8)
+        uint32_t *o = (uint32_t *)r.out_rgba + pix;
         if (word == ~0ull) {
-            o[0] = r.background[0]; o[1] = r.background[1];
-            o[2] = r.background[2]; o[3] = r.background[3];
+            *o = rgba(r.background[0], r.background[1], r.background[2], r.background[3]);
             bg++;
             continue;
         }
@@ -151,7 +160,7 @@ __global__ void k_resolve(const curast_resolve_t r) {
         double t = (d00 * we2 - d01 * we1) / den;
         if (!ok) {
             degen++;
-            o[0] = 255; o[1] = 0; o[2] = 255; o[3] = 255;
+            *o = rgba(255, 0, 255, 255);
             shaded++;
             continue;
         }
@@ -227,11 +236,13 @@ __global__ void k_resolve(const curast_resolve_t r) {
             double sh = 0.2 + 0.8 * ndl;
             col[0] *= sh; col[1] *= sh; col[2] *= sh;
         }
+        uint32_t q8[4];
         for (int c = 0; c < 4; ++c) {
             double q = rint(col[c]);
             q = fmin(fmax(q, 0.0), 255.0);
-            o[c] = (uint8_t)q;
+            q8[c] = (uint32_t)q;
         }
+        *o = rgba(q8[0], q8[1], q8[2], q8[3]);
         shaded++;
     }
     atomicAdd(&s_cnt[0], shaded);
@@ -242,9 +253,46 @@ __global__ void k_resolve(const curast_resolve_t r) {
         atomicAdd((unsigned long long *)(r.counters + threadIdx.x), s_cnt[threadIdx.x]);
 }
 
-// box filter with floor rounding (resolvepass.py:398-407)
-__global__ void k_downsample(const uint8_t *__restrict__ src, int64_t w, int64_t h, int factor,
+// box filter with floor rounding (resolvepass.py:398-407): one thread per
+// output pixel, a source row of `factor` RGBA8 pixels as one 4/8/16-byte
+// load, the four channels summed in registers, one 32-bit store
+template <int FACTOR>
+__global__ void k_downsample(const uint8_t *__restrict__ src, int64_t w, int64_t h,
                              uint8_t *__restrict__ dst) {
+    const int64_t ow = w / FACTOR, oh = h / FACTOR;
+    const int64_t n = ow * oh;
+    const uint32_t *s32 = (const uint32_t *)src;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = p % ow, oy = p / ow;
+        uint32_t sum[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int dy = 0; dy < FACTOR; ++dy) {
+            const uint32_t *row = s32 + (oy * FACTOR + dy) * w + ox * FACTOR;
+            uint32_t px[FACTOR];
+            if (FACTOR == 4) {
+                const uint4 v = __ldg((const uint4 *)row);
+                px[0] = v.x; px[1] = v.y; px[2 % FACTOR] = v.z; px[3 % FACTOR] = v.w;
+            } else if (FACTOR == 2) {
+                const uint2 v = __ldg((const uint2 *)row);
+                px[0] = v.x; px[1 % FACTOR] = v.y;
+            } else {
+#pragma unroll
+                for (int dx = 0; dx < FACTOR; ++dx) px[dx] = __ldg(row + dx);
+            }
+#pragma unroll
+            for (int dx = 0; dx < FACTOR; ++dx)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) sum[c] += (px[dx] >> (8 * c)) & 0xffu;
+        }
+        constexpr uint32_t d = FACTOR * FACTOR;
+        ((uint32_t *)dst)[p] = (sum[0] / d) | ((sum[1] / d) << 8) | ((sum[2] / d) << 16) |
+                               ((sum[3] / d) << 24);
+    }
+}
+
+__global__ void k_downsample_any(const uint8_t *__restrict__ src, int64_t w, int64_t h, int factor,
+                                 uint8_t *__restrict__ dst) {
     const int64_t ow = w / factor, oh = h / factor;
     const int64_t n = ow * oh * 4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -258,7 +306,6 @@ __global__ void k_downsample(const uint8_t *__restrict__ src, int64_t w, int64_t
         dst[i] = (uint8_t)(sum / (uint32_t)(factor * factor));
     }
 }
-
 
 int sms() {
     int dev = 0, n = 0;
@@ -455,7 +502,10 @@ int curast_debug_view(const curast_debug_t *d, void *stream) {
 int curast_downsample(const uint8_t *src, int64_t w, int64_t h, int32_t factor, uint8_t *dst,
                       void *stream) {
     if (!src || !dst || factor < 1 || w % factor || h % factor) return CURAST_E_INVALID;
-    k_downsample<<<sms() * 4, 256, 0, (cudaStream_t)stream>>>(src, w, h, factor, dst);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (factor == 2 && ((uintptr_t)src & 7) == 0) k_downsample<2><<<sms() * 8, 256, 0, st>>>(src, w, h, dst);
+    else if (factor == 4 && ((uintptr_t)src & 15) == 0) k_downsample<4><<<sms() * 8, 256, 0, st>>>(src, w, h, dst);
+    else k_downsample_any<<<sms() * 4, 256, 0, st>>>(src, w, h, factor, dst);
     return cudaGetLastError() == cudaSuccess ? 0 : CURAST_E_CUDA;
 }
 

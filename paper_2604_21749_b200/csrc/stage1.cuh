@@ -14,7 +14,6 @@ constexpr int W_THREADS = 256;
 constexpr int W_WARPS = W_THREADS / 32;
 constexpr int W_TPL = 4;                       // consecutive triangles per lane per step
 constexpr int W_STEP = 32 * W_TPL;             // triangles per warp step
-constexpr int W_CHUNK = kS1Chunk;              // triangles per warp claim
 constexpr int W_QCAP = 32 + W_STEP;            // per-warp fp64 queue
 
 struct FilterPairs {
@@ -189,9 +188,9 @@ __global__ void __launch_bounds__(W_THREADS, MINB) k_s1_cull(const curast_frame_
             if (c < total) {
                 int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
                 item = __ldg(f.unit_index + u);
-                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * W_CHUNK;
+                lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * f.chunk_tris;
                 hi = __ldg(f.unit_hi + u);
-                hi = lo + W_CHUNK < hi ? lo + W_CHUNK : hi;
+                hi = lo + f.chunk_tris < hi ? lo + f.chunk_tris : hi;
             }
         }
         c = __shfl_sync(0xffffffffu, c, 0);

@@ -40,6 +40,17 @@ __device__ __forceinline__ void lean_load_step(LeanConsts &F, const float *p) {
     F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
 }
 
+// lean_load from a shared-memory copy of the filter block.
+__device__ __forceinline__ void lean_load_smem(LeanConsts &F, const float4 *q) {
+    const float4 a = q[0], b = q[1], c = q[2], d = q[3];
+    F.cx = make_float2(a.x, b.x);
+    F.cy = make_float2(a.y, b.y);
+    F.cz = make_float2(a.z, b.z);
+    F.c3 = make_float2(a.w, b.w);
+    F.dx = c.x; F.dy = c.y; F.dz = c.z; F.d3 = c.w;
+    F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
+}
+
 // One projected vertex (filter units): P = (X', Y') / d', D = d'.
 struct PV {
     float2 P;
@@ -122,18 +133,21 @@ __device__ __forceinline__ unsigned tri_full(const PV &a, const PV &b, const PV 
     return (is_tiny || is_fr) ? (is_fr ? 2u : 0u) : 1u;
 }
 
-// Vertex-ref patterns of a lane's 4 triangles (refs 3t..3t+2):
+// Vertex-ref patterns of a lane's 4 triangles (refs 3t..3t+2), two quads of
+// a strip in the two triangulations of the benchmark generators:
 //   0 generic: 12 gathered vertices, triangle t = (3t, 3t+1, 3t+2)
-//   1 grid quads (a,c,b),(b,c,d): distinct refs 0,1,2,5,8,11 = U0..U5,
+//   1 grid quads (a,c,b),(b,c,d) (make_tessellated_quad, scenedesc.py:207-214):
+//     distinct refs 0,1,2,5,8,11 = U0..U5,
 //     triangles (U0,U1,U2) (U2,U1,U3) (U2,U3,U4) (U4,U3,U5)
-//   2 sphere quads (a,b,c),(b,d,c): distinct refs 0,1,2,4,7,10,
-//     triangles (U0,U1,U2) (U1,U3,U2) (U1,U4,U3) (U4,U5,U3)
+//   2 sphere quads (a,d,c),(a,b,d) (make_sphere, scenedesc.py:218-245):
+//     distinct refs 0,1,2,4,7,10 = U0..U5,
+//     triangles (U0,U1,U2) (U0,U3,U1) (U3,U4,U1) (U3,U5,U4)
 // (each triangle's vertex order is irrelevant: the bbox tests are symmetric)
 __device__ __forceinline__ int strip_kind(const uint32_t *ix, bool full) {
     const bool gq = full && ix[3] == ix[2] && ix[4] == ix[1] && ix[6] == ix[2] &&
                     ix[7] == ix[5] && ix[9] == ix[8] && ix[10] == ix[5];
-    const bool sq = full && ix[3] == ix[1] && ix[5] == ix[2] && ix[6] == ix[1] &&
-                    ix[8] == ix[4] && ix[9] == ix[7] && ix[11] == ix[4];
+    const bool sq = full && ix[3] == ix[0] && ix[5] == ix[1] && ix[6] == ix[4] &&
+                    ix[8] == ix[1] && ix[9] == ix[4];
     return __all_sync(0xffffffffu, gq) ? 1 : (__all_sync(0xffffffffu, sq) ? 2 : 0);
 }
 
@@ -143,13 +157,13 @@ __host__ __device__ constexpr int strip_r(int kind, int k) {
     return k < 3 ? k : (kind == 1 ? 3 * k - 4 : 3 * k - 5);
 }
 __host__ __device__ constexpr int strip_g(int kind, int k) {
-    // kind 1: 0 1 2 | 2 1 3 | 2 3 4 | 4 3 5    kind 2: 0 1 2 | 1 3 2 | 1 4 3 | 4 5 3
+    // kind 1: 0 1 2 | 2 1 3 | 2 3 4 | 4 3 5    kind 2: 0 1 2 | 0 3 1 | 3 4 1 | 3 5 4
     return kind == 1 ? (k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 2 : k == 4 ? 1 :
                         k == 5 ? 3 : k == 6 ? 2 : k == 7 ? 3 : k == 8 ? 4 : k == 9 ? 4 :
                         k == 10 ? 3 : 5)
-                     : (k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 1 : k == 4 ? 3 :
-                        k == 5 ? 2 : k == 6 ? 1 : k == 7 ? 4 : k == 8 ? 3 : k == 9 ? 4 :
-                        k == 10 ? 5 : 3);
+                     : (k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 0 : k == 4 ? 3 :
+                        k == 5 ? 1 : k == 6 ? 3 : k == 7 ? 4 : k == 8 ? 1 : k == 9 ? 3 :
+                        k == 10 ? 5 : 4);
 }
 static_assert(strip_r(1, 3) == 5 && strip_r(1, 5) == 11 && strip_r(2, 3) == 4 &&
               strip_r(2, 5) == 10, "strip refs");
@@ -234,9 +248,9 @@ __device__ __forceinline__ bool claim_flat(const curast_frame_t &f, int lane, in
         if (c < total) {
             const int64_t u = upper_index(f.unit_chunk_prefix, f.n_units + 1, c);
             item = __ldg(f.unit_index + u);
-            lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * kS1Chunk;
+            lo = __ldg(f.unit_lo + u) + (c - __ldg(f.unit_chunk_prefix + u)) * f.chunk_tris;
             hi = __ldg(f.unit_hi + u);
-            hi = lo + kS1Chunk < hi ? lo + kS1Chunk : hi;
+            hi = lo + f.chunk_tris < hi ? lo + f.chunk_tris : hi;
         }
     }
     c = __shfl_sync(0xffffffffu, c, 0);
@@ -355,6 +369,175 @@ __global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
             else
                 v2_step<0>(f, F, pb, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
                            lt_mask);
+        }
+    }
+    qx_reserve_close(f, R, lane);
+    unsigned long long cnt[2] = {cnt16 & 0xffffu, cnt16 >> 16};
+    flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+    flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+}
+
+// ------------------------------------------------ instanced (node groups)
+// Instanced stage 1 (kernels.py:205-254, pipeline.py:244: the work space is
+// the unique triangles of the node groups).  A work unit is a 2048-triangle
+// chunk of a group's mesh under a block of CURAST_INST_BLOCK instances: the
+// warp copies the block's filter rows to shared memory once, then per
+// 128-triangle step loads the indices and gathers the (strip-shared)
+// vertices ONCE and runs the projection / lane bound / decisions for every
+// instance from registers + shared memory — no global load in the instance
+// loop.  Undecided (instance, triangle) pairs go to the fp64 queue with their
+// object-space positions and the instance's item in the tag.
+template <int KIND>
+__device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (*sF)[4],
+                                         const long long *sItem, int ninst,
+                                         const float4 *__restrict__ pb, const uint32_t *ix,
+                                         int nv, long long local0, float W, float H, float slack,
+                                         bool tiny, unsigned &cnt16, QxReserve &R,
+                                         unsigned long long *qcount, int lane,
+                                         unsigned lt_mask) {
+    const unsigned vmask = (1u << nv) - 1u;
+    if constexpr (KIND == 0) {
+        // generic lanes: triangle by triangle, every instance per triangle
+#pragma unroll 1
+        for (int t = 0; t < 4; ++t) {
+            const float4 a = __ldg(pb + ix[3 * t]), b = __ldg(pb + ix[3 * t + 1]),
+                         c = __ldg(pb + ix[3 * t + 2]);
+            const float x[3] = {a.x, b.x, c.x}, y[3] = {a.y, b.y, c.y}, z[3] = {a.z, b.z, c.z};
+            const bool valid = (vmask >> t) & 1u;
+#pragma unroll 1
+            for (int k = 0; k < ninst; ++k) {
+                LeanConsts F;
+                lean_load_smem(F, sF[k]);
+                const unsigned r = lean_bits(F, x, y, z, W, H, slack, tiny);
+                const bool need = valid && (r & 1u);
+                const bool fr = valid && (r & 2u);
+                cnt16 += (unsigned)fr + ((unsigned)(valid && r == 0u) << 16);
+                const unsigned bb = __ballot_sync(0xffffffffu, need);
+                if (bb) {
+                    const QxSlots qs = qx_reserve(R, qcount, __popc(bb), lane);
+                    if (need)
+                        qx_put(f, qs.at(__popc(bb & lt_mask)), make_float3(a.x, a.y, a.z),
+                               make_float3(b.x, b.y, b.z), make_float3(c.x, c.y, c.z),
+                               (sItem[k] << 40) | (local0 + t));
+                }
+            }
+        }
+    } else {
+    float3 p[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const float4 q = __ldg(pb + ix[strip_r(KIND, k)]);
+        p[k] = make_float3(q.x, q.y, q.z);
+    }
+#pragma unroll 1
+    for (int k = 0; k < ninst; ++k) {
+        LeanConsts F;
+        lean_load_smem(F, sF[k]);
+        PV v[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) v[j] = pv_project(F, make_float4(p[j].x, p[j].y, p[j].z, 0.f));
+        const unsigned bits = strip_bits<KIND>(F, v, W, H, slack, tiny);
+        const unsigned need = bits & vmask, fr = (bits >> 4) & vmask;
+        cnt16 += (unsigned)__popc(fr) + ((unsigned)(nv - __popc(need) - __popc(fr)) << 16);
+        unsigned b[4];
+        int tot = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            b[t] = __ballot_sync(0xffffffffu, (need >> t) & 1u);
+            tot += __popc(b[t]);
+        }
+        if (!tot) continue;
+        const QxSlots qs = qx_reserve(R, qcount, tot, lane);
+        const long long tag = (sItem[k] << 40) | local0;
+        const long long flag = (bits & 0x100u) ? CURAST_QX_INTERIOR : 0ll;
+        int base = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if ((need >> t) & 1u)
+                qx_put(f, qs.at(base + __popc(b[t] & lt_mask)), p[strip_g(KIND, 3 * t)],
+                       p[strip_g(KIND, 3 * t + 1)], p[strip_g(KIND, 3 * t + 2)],
+                       (tag + t) | flag);
+            base += __popc(b[t]);
+        }
+    }
+    }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_s1i_v2(const curast_frame_t f) {
+    constexpr int STEP = 128;
+    __shared__ float4 sF[8][CURAST_INST_BLOCK][4];
+    __shared__ long long sItem[8][CURAST_INST_BLOCK];
+    __shared__ QxReserve sres[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    unsigned cnt16 = 0;
+    const float W = (float)f.width, H = (float)f.height;
+    const float slack = (float)(f.width > f.height ? f.width : f.height) * 1.4551915e-11f;
+    const bool tiny = f.tiny_cull != 0;
+    const int64_t CHUNK = f.inst_chunk_tris;
+    const int64_t total = __ldg(f.inst_unit_chunk_prefix + f.n_inst_units);
+    unsigned long long *qcount = (unsigned long long *)(f.counters + CURAST_C_QX);
+    QxReserve &R = sres[w];
+    if (lane == 0) R = QxReserve{0u, 0};
+    __syncwarp();
+    for (;;) {
+        long long c = 0, g = 0, lo = 0, hi = 0;
+        if (lane == 0) {
+            c = (long long)atomicAdd((unsigned long long *)(f.counters + CURAST_C_CLAIM1I), 1ull);
+            if (c < total) {
+                const int64_t u = upper_index(f.inst_unit_chunk_prefix, f.n_inst_units + 1, c);
+                g = __ldg(f.inst_unit_index + u);
+                lo = __ldg(f.inst_unit_lo + u) + (c - __ldg(f.inst_unit_chunk_prefix + u)) * CHUNK;
+                hi = __ldg(f.inst_unit_hi + u);
+                hi = lo + CHUNK < hi ? lo + CHUNK : hi;
+            }
+        }
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= total) break;
+        g = __shfl_sync(0xffffffffu, g, 0);
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        hi = __shfl_sync(0xffffffffu, hi, 0);
+        if (__any_sync(0xffffffffu, cnt16 & 0x80008000u)) {
+            unsigned long long cnt[2] = {cnt16 & 0xffffu, cnt16 >> 16};
+            flush_stats(f.counters + CURAST_C_S1 + CULL_FRUSTUM, cnt, 1);
+            flush_stats(f.counters + CURAST_C_S1 + CULL_TINY, cnt + 1, 1);
+            cnt16 = 0;
+        }
+        // unit = group | first instance << 32 (CURAST_INST_BLOCK instances)
+        const int64_t k0 = g >> 32;
+        g &= 0xFFFFFFFFll;
+        const int64_t ioff = __ldg(f.group_item_off + g);
+        const int ninst = (int)(min(__ldg(f.group_item_count + g), k0 + CURAST_INST_BLOCK) - k0);
+        // the block's instances: items and filter rows into shared memory
+        __syncwarp();
+        if (lane < ninst) sItem[w][lane] = __ldg(f.group_items + ioff + k0 + lane);
+        __syncwarp();
+        for (int j = lane; j < 4 * ninst; j += 32)
+            sF[w][j >> 2][j & 3] =
+                __ldg((const float4 *)(f.item_filter + CURAST_FILTER_FLOATS * sItem[w][j >> 2]) +
+                      (j & 3));
+        __syncwarp();
+        const int64_t first = sItem[w][0];
+        const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + first);
+        const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + first) + 3 * lo;
+        const int n = (int)(hi - lo);
+        const bool vec = (((uintptr_t)ib) & 15) == 0;
+        for (int s0 = 0; s0 < n; s0 += STEP) {
+            const int o = s0 + 4 * lane;
+            const int nv = max(0, min(4, n - o));
+            uint32_t ix[12];
+            load_step_indices(ib, o, nv, vec, ix);
+            const int kind = strip_kind(ix, nv == 4);
+            if (kind == 1)
+                v2i_step<1>(f, sF[w], sItem[w], ninst, pb, ix, nv, lo + o, W, H, slack, tiny,
+                            cnt16, R, qcount, lane, lt_mask);
+            else if (kind == 2)
+                v2i_step<2>(f, sF[w], sItem[w], ninst, pb, ix, nv, lo + o, W, H, slack, tiny,
+                            cnt16, R, qcount, lane, lt_mask);
+            else
+                v2i_step<0>(f, sF[w], sItem[w], ninst, pb, ix, nv, lo + o, W, H, slack, tiny,
+                            cnt16, R, qcount, lane, lt_mask);
         }
     }
     qx_reserve_close(f, R, lane);

@@ -150,12 +150,6 @@ class DeviceMesh:
             return g[:3] + (q + 0.5) / 65536.0 * g[3:]
         raise ValueError("unsupported position conversion")
 
-    def index_steps(self):
-        """Lane-major index steps of the u32 stream (built once)."""
-        if getattr(self, "_index_steps", None) is None:
-            self._index_steps = build_index_steps(self.indices_u32(), self.triangle_count)
-        return self._index_steps
-
     def indices_u32(self):
         if self.idx_format == N.IDX_U32:
             return self.indices
@@ -169,21 +163,6 @@ class DeviceMesh:
         win = lo | (hi << 32)
         rel = (win >> (bit & 31)) & ((1 << b) - 1) if b < 63 else win
         return (rel + mn).to(torch.int64).to(torch.int32)
-
-
-def build_index_steps(indices: torch.Tensor, triangle_count: int) -> torch.Tensor:
-    """Lane-major index steps (curast.h indices_ilv): per step of
-    CURAST_STEP_TRIS = 128 triangles 384 words, lane l holding triangles
-    l + 32k (k < 4, zero padded past the mesh) as 3 consecutive indices each."""
-    MT = N.STEP_TRIS
-    T = int(triangle_count)
-    ns = -(-T // MT)
-    dev = indices.device
-    if ns == 0:
-        return torch.zeros(0, dtype=torch.int32, device=dev)
-    x = torch.zeros((ns * MT, 3), dtype=torch.int32, device=dev)
-    x[:T] = indices[:3 * T].view(T, 3)
-    return x.view(ns, 4, 32, 3).permute(0, 2, 1, 3).contiguous().view(-1)
 
 
 _CACHE_ATTR = "_curast_device_copies"
@@ -255,24 +234,7 @@ class SceneGeometry:
         else:
             self.positions = torch.cat(pos_parts)
             self.indices = torch.cat(idx_parts)
-        # lane-major index steps (built on first use, SceneGeometry.index_steps)
-        self.ilv_off = [0] * len(dms)
-        self.indices_ilv = None
         self.keepalive = dms
-
-    def index_steps(self):
-        """Lane-major index steps of every mesh (curast.h indices_ilv) for the
-        f32 / u32 per-triangle kernel; None for other formats."""
-        if self.indices_ilv is None and self.pos_format == N.POS_F32 \
-                and self.idx_format == N.IDX_U32:
-            parts, nw = [], 0
-            for k, d in enumerate(self.meshes):
-                st = d.index_steps()
-                self.ilv_off[k] = nw
-                parts.append(st)
-                nw += st.numel()
-            self.indices_ilv = parts[0] if len(parts) == 1 else torch.cat(parts)
-        return self.indices_ilv
 
 
 _scene_cache: dict = {}

@@ -194,6 +194,35 @@ def shard_items(ctx: RenderContext, work_range, inst_kernel: bool) -> np.ndarray
     return mask
 
 
+def _span(starts: np.ndarray, counts: np.ndarray, begin: int, end: int) -> np.ndarray:
+    """Triangles of each unit inside [begin, end) of the work space."""
+    return np.maximum(np.minimum(starts + counts, end) - np.maximum(starts, begin), 0)
+
+
+# work chunks per resident warp the chunk size aims for (load balance of the
+# persistent stage-1 kernels: 148 SMs x 32 warps)
+CHUNKS_PER_WARP = 4
+
+
+def _target_chunks(device) -> int:
+    try:
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+    except Exception:
+        sms = 148
+    return CHUNKS_PER_WARP * 32 * sms
+
+
+def _choose_chunk(work: int, chunk_max: int, quantum: int, target: int) -> int:
+    """Largest power-of-two multiple of ``quantum`` up to ``chunk_max`` that
+    still splits ``work`` triangles into ``target`` chunks (streamed frames
+    keep 2048-triangle chunks; small frames get more, smaller ones so every
+    SM has work)."""
+    c = chunk_max
+    while c > quantum and work < target * c:
+        c //= 2
+    return max(quantum, c)
+
+
 def _work_table(starts: np.ndarray, counts: np.ndarray, unit_ids: np.ndarray,
                 begin: int, end: int, chunk: int):
     """Units (items or groups) intersected with [begin, end) of their global
@@ -212,22 +241,14 @@ def _work_table(starts: np.ndarray, counts: np.ndarray, unit_ids: np.ndarray,
     return ids.astype(np.int64), lo_l.astype(np.int64), hi_l.astype(np.int64), cp
 
 
-# unique geometry above this is streamed once per frame by the instanced
-# stage-1 kernel instead of once per instance by the flat one
-INST_KERNEL_MIN_BYTES = 96 << 20
-
-
 def _instanced_kernel_preferred(geo) -> bool:
-    env = os.environ.get("CURAST_INSTANCED_KERNEL")
-    if env in ("0", "1"):
-        return env == "1"
-    if geo.pos_format != N.POS_F32 or geo.idx_format != N.IDX_U32:
-        # compressed / f64 formats: the generic flat kernel decodes every
-        # instance's copy (config Dq: flat 10.2 ms vs instanced 8.8 ms)
-        return True
-    nbytes = int(geo.positions.numel()) * geo.positions.element_size() + \
-        int(geo.indices.numel()) * geo.indices.element_size()
-    return nbytes > INST_KERNEL_MIN_BYTES
+    """Instanced frames run the instanced stage-1 kernels (a unique
+    triangle's vertices fetched once per block of 16 instances) unless
+    CURAST_INSTANCED_KERNEL=0 selects the flat table over the items (same
+    words and counters: instancing == flat, test_rasterpipe.py:186-203).
+    Measured on config D (1M-triangle sphere x 998 instances): instanced
+    3.69 ms vs flat 4.05 ms stage 1 (profiles/r02_configs.jsonl)."""
+    return os.environ.get("CURAST_INSTANCED_KERNEL", "1") != "0"
 
 
 class PreparedFrame:
@@ -295,21 +316,20 @@ class PreparedFrame:
                            self.height, float(camera.near), geo.pos_format)
 
         # Stage-1 kernel for instanced frames: the instanced one (a unique
-        # triangle fetched once, tested under every instance) or the flat one
-        # over the items (same words and counters: instancing == flat,
-        # test_rasterpipe.py:186-203).  Measured on config D (18 MB of unique
-        # f32 / u32 geometry, L2-resident): flat 5.35 ms vs instanced 7.64
-        # ms, so the flat table is used for full frames whose unique lean-
-        # format geometry fits the L2 budget; sharded frames keep the
-        # instanced work space, whose work ranges count unique triangles
-        # (pipeline.py:244).
+        # triangle fetched once, tested under every instance) or, with
+        # CURAST_INSTANCED_KERNEL=0, the flat one over the items (same words
+        # and counters); sharded frames keep the instanced work space, whose
+        # work ranges count unique triangles (pipeline.py:244).
         self.inst_kernel = self.instanced and (
             work_range is not None or _instanced_kernel_preferred(geo))
         if work_range is None:
             work_range = (0, int(ctx.group_prefix[-1]) if self.inst_kernel else self.total)
         self.work_range = (int(work_range[0]), int(work_range[1]))
-        chunk = int(_lib.curast_chunk_tris(0))
-        ichunk = int(_lib.curast_chunk_tris(1))
+        chunk_max = int(_lib.curast_chunk_tris(0))
+        ichunk_max = int(_lib.curast_chunk_tris(1))
+        quantum = int(_lib.curast_chunk_quantum())
+        target = _target_chunks(device)
+        lo_w, hi_w = self.work_range
         if self.inst_kernel:
             # work space = unique triangles of the node groups (pipeline.py:244);
             # single-instance groups stream through the flat kernel
@@ -318,8 +338,6 @@ class PreparedFrame:
             tris = np.diff(ctx.group_prefix)
             single = ctx.group_item_count == 1
             first_item = ctx.group_items[ctx.group_item_off] if ng else np.zeros(0, np.int64)
-            u = _work_table(starts[single], tris[single], first_item[single],
-                            *self.work_range, chunk)
             # multi-instance groups: one unit per block of CURAST_INST_BLOCK
             # instances (unit id = group | first_instance << 32)
             multi = np.nonzero(~single)[0]
@@ -327,29 +345,33 @@ class PreparedFrame:
             rep_g = np.repeat(multi, nkb)
             kb = np.concatenate([np.arange(k) for k in nkb]) if len(nkb) else np.zeros(0, np.int64)
             ids = rep_g.astype(np.int64) | ((kb.astype(np.int64) * INST_BLOCK) << 32)
+            ninst = np.minimum(ctx.group_item_count[rep_g] - kb * INST_BLOCK, INST_BLOCK)
+            span_s = _span(starts[single], tris[single], lo_w, hi_w)
+            span_m = _span(starts[rep_g], tris[rep_g], lo_w, hi_w)
+            chunk = _choose_chunk(int(span_s.sum()), chunk_max, quantum, target)
+            # an instanced unit costs its triangles x its instances
+            ichunk = _choose_chunk(int((span_m * ninst).sum()) // INST_BLOCK, ichunk_max,
+                                   quantum, target)
+            u = _work_table(starts[single], tris[single], first_item[single],
+                            *self.work_range, chunk)
             v = _work_table(starts[rep_g], tris[rep_g], ids, *self.work_range, ichunk)
         else:
             counts = np.diff(ctx.prefix)
+            chunk = _choose_chunk(int(_span(ctx.prefix[:-1], counts, lo_w, hi_w).sum()),
+                                  chunk_max, quantum, target)
+            ichunk = ichunk_max
             u = _work_table(ctx.prefix[:-1], counts, np.arange(n), *self.work_range, chunk)
             v = (np.zeros(0, np.int64),) * 3 + (np.zeros(1, np.int64),)
+        self.chunk, self.ichunk = chunk, ichunk
         self.unit_index, self.unit_lo, self.unit_hi, self.unit_cp = u
         self.iunit_index, self.iunit_lo, self.iunit_hi, self.iunit_cp = v
 
-        # lane-major index steps: measured faster for instanced scenes whose
-        # geometry is L2-resident (config D 5.37 -> 5.14 ms stage 1) and
-        # slower for streamed geometry (config B 0.833 -> 0.877 ms)
-        use_ilv = (self.instanced and not self.inst_kernel
-                   and os.environ.get("CURAST_ILV", "auto") != "0") \
-            or os.environ.get("CURAST_ILV") == "1"
-        ilv = geo.index_steps() if use_ilv else None
-        ilv_off = np.asarray([geo.ilv_off[g] if g >= 0 else 0 for g in gslot], dtype=np.int64)
         up = PackedUpload()
         k_prefix = up.add(ctx.prefix)
         k_mv = up.add(ctx.item_mv.reshape(-1))
         k_mw = up.add(ctx.item_mw.reshape(-1))
         k_vo = up.add(vtx_off)
         k_io = up.add(idx_off)
-        k_lo = up.add(ilv_off)
         k_f = up.add(filt.reshape(-1))
         k_q = up.add(qgrid.reshape(-1).astype(np.float64))
         k_pk = up.add(pack.reshape(-1))
@@ -383,9 +405,6 @@ class PreparedFrame:
         f.item_filter = up.ptr(k_f)
         f.item_qgrid = up.ptr(k_q)
         f.item_pack = up.ptr(k_pk)
-        if ilv is not None:
-            f.item_ilv_off = up.ptr(k_lo)
-            f.indices_ilv = ilv.data_ptr()
         f.instanced = int(self.inst_kernel)
         f.use_filter = int(self.use_filter)
         f.n_groups = len(ctx.group_item_count)
@@ -398,14 +417,14 @@ class PreparedFrame:
         f.unit_lo = up.ptr(k_ul)
         f.unit_hi = up.ptr(k_uh)
         f.unit_chunk_prefix = up.ptr(k_uc)
-        f.chunk_tris = chunk
+        f.chunk_tris = self.chunk
         f.flat_chunks = int(self.unit_cp[-1])
         f.n_inst_units = len(self.iunit_index)
         f.inst_unit_index = up.ptr(k_vi)
         f.inst_unit_lo = up.ptr(k_vl)
         f.inst_unit_hi = up.ptr(k_vh)
         f.inst_unit_chunk_prefix = up.ptr(k_vc)
-        f.inst_chunk_tris = ichunk
+        f.inst_chunk_tris = self.ichunk
         f.p0, f.p1, f.near = p0, p1, float(camera.near)
         f.width, f.height = self.width, self.height
         view = np.asarray(camera.view_transform, dtype=np.float64)

@@ -1,7 +1,7 @@
 """Every stage-1 route the host can select renders bit-exact frames: the
-streamed flat filter (k_s1_v2), the lane-major index steps (k_s1_lean_ilv,
-CURAST_ILV=1), the instanced kernel (CURAST_INSTANCED_KERNEL=1) and the
-no-filter route (CURAST_FILTER=0: every triangle through the fp64 pass) —
+streamed flat filter (k_s1_v2), the instanced kernel (k_s1i_v2, default for
+instanced frames) or the flat table for them (CURAST_INSTANCED_KERNEL=0),
+and the no-filter route (CURAST_FILTER=0: every triangle through the fp64 pass) —
 golden fixtures, random scenes and a grid against the stored reference words
 / the oracle.  The routes are chosen on the host when a frame is prepared, so
 each runs in its own process."""
@@ -53,8 +53,6 @@ sys.exit(1 if bad else 0)
 
 @pytest.mark.parametrize("env", [
     {},
-    {"CURAST_ILV": "1"},
-    {"CURAST_ILV": "0"},
     {"CURAST_INSTANCED_KERNEL": "1"},
     {"CURAST_INSTANCED_KERNEL": "0"},
     {"CURAST_FILTER": "0"},

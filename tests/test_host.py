@@ -242,25 +242,18 @@ def test_device_copy_cache_is_identity_checked():
     assert dv.device_mesh(m, cpu) is not b
 
 
-def test_build_index_steps_lane_major_layout():
-    """device.build_index_steps (curast.h indices_ilv): per 128-triangle
-    step, lane l's 12 words are triangles l, l+32, l+64, l+96 (3 indices
-    each), zero past the mesh."""
-    import torch
-
-    from paper_2604_21749_b200 import device as dv
-    for T in (1, 127, 128, 300):
-        idx = (np.arange(3 * T, dtype=np.uint32) * 7 + 1)
-        st = dv.build_index_steps(torch.from_numpy(idx.view(np.int32)), T).numpy().view(np.uint32)
-        ns = -(-T // 128)
-        assert st.size == ns * 384
-        w = st.reshape(ns, 32, 4, 3)
-        for s_ in range(ns):
-            for lane in range(32):
-                for k in range(4):
-                    t = s_ * 128 + lane + 32 * k
-                    want = idx[3 * t:3 * t + 3] if t < T else np.zeros(3, np.uint32)
-                    assert np.array_equal(w[s_, lane, k], want)
+def test_chunk_size_balances_small_frames():
+    """pipeline._choose_chunk: 2048-triangle chunks for streamed frames, down
+    to 128 so a small frame still gives every resident warp several chunks."""
+    from paper_2604_21749_b200.pipeline import _choose_chunk
+    target = 4 * 32 * 148
+    assert _choose_chunk(99_998_082, 2048, 128, target) == 2048
+    assert _choose_chunk(999_698, 2048, 128, target) == 128
+    assert _choose_chunk(10_078_880, 2048, 128, target) == 512
+    assert _choose_chunk(0, 2048, 128, target) == 128
+    for w in (1, 10 ** 5, 3 * 10 ** 6, 10 ** 9):
+        c = _choose_chunk(w, 2048, 128, target)
+        assert c % 128 == 0 and 128 <= c <= 2048
 
 
 def _grazing_transforms(rng, cam, n):
