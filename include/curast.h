@@ -77,7 +77,8 @@ enum curast_error {
 };
 
 /* Per-item fp32 filter block: 16 floats per draw item (host computed).
- *   [0..3]  X = px*d affine row   [4..7]  Y = py*d row   [8..11] d row
+ *   [0..7]  X = px*d and Y = py*d affine rows interleaved: X0 Y0 X1 Y1 X2 Y2
+ *           X3 Y3 (coefficients of x, y, z, 1)   [8..11] d row
  *   [12] E_xy  [13] E_d  (absolute error bounds of the fp32 rows)
  *   [14] near_hi (d above which the near tests are decided)  [15] unused  */
 #define CURAST_FILTER_FLOATS 16

@@ -46,11 +46,14 @@ struct FilterConsts {
     float exy, ed, near_hi;
 };
 
+// The block's (X, Y) rows are stored interleaved (curast.h
+// CURAST_FILTER_FLOATS): X0 Y0 X1 Y1 | X2 Y2 X3 Y3 | d0 d1 d2 d3 | E_xy E_d
+// near_hi -, so a lane's 128-bit loads give FFMA2-ready register pairs.
 __device__ __forceinline__ void load_filter(FilterConsts &F, const float *__restrict__ p) {
     const float4 *q = (const float4 *)p;
     float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
-    F.c[0] = a.x; F.c[1] = a.y; F.c[2] = a.z; F.c[3] = a.w;
-    F.c[4] = b.x; F.c[5] = b.y; F.c[6] = b.z; F.c[7] = b.w;
+    F.c[0] = a.x; F.c[1] = a.z; F.c[2] = b.x; F.c[3] = b.z;
+    F.c[4] = a.y; F.c[5] = a.w; F.c[6] = b.y; F.c[7] = b.w;
     F.c[8] = c.x; F.c[9] = c.y; F.c[10] = c.z; F.c[11] = c.w;
     F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
 }
@@ -102,15 +105,19 @@ struct LeanConsts {
     float exy, ed, near_hi;
 };
 
-__device__ __forceinline__ void lean_load(LeanConsts &F, const float *__restrict__ p) {
-    const float4 *q = (const float4 *)p;
-    const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
-    F.cx = make_float2(a.x, b.x);
-    F.cy = make_float2(a.y, b.y);
-    F.cz = make_float2(a.z, b.z);
-    F.c3 = make_float2(a.w, b.w);
+__device__ __forceinline__ void lean_from(LeanConsts &F, const float4 &a, const float4 &b,
+                                          const float4 &c, const float4 &d) {
+    F.cx = make_float2(a.x, a.y);
+    F.cy = make_float2(a.z, a.w);
+    F.cz = make_float2(b.x, b.y);
+    F.c3 = make_float2(b.z, b.w);
     F.dx = c.x; F.dy = c.y; F.dz = c.z; F.d3 = c.w;
     F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
+}
+
+__device__ __forceinline__ void lean_load(LeanConsts &F, const float *__restrict__ p) {
+    const float4 *q = (const float4 *)p;
+    lean_from(F, __ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(q + 3));
 }
 
 // Projected triangle: P[k] = (px', py') with |px' - px64| <= eps per

@@ -25,10 +25,10 @@ struct FilterPairs {
 __device__ __forceinline__ void load_filter_pairs(FilterPairs &F, const float *__restrict__ p) {
     const float4 *q = (const float4 *)p;
     float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
-    F.cx = make_float2(a.x, b.x);
-    F.cy = make_float2(a.y, b.y);
-    F.cz = make_float2(a.z, b.z);
-    F.c3 = make_float2(a.w, b.w);
+    F.cx = make_float2(a.x, a.y);   // interleaved (X, Y) rows (filter.cuh)
+    F.cy = make_float2(a.z, a.w);
+    F.cz = make_float2(b.x, b.y);
+    F.c3 = make_float2(b.z, b.w);
     F.dx = c.x; F.dy = c.y; F.dz = c.z; F.d3 = c.w;
     F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
 }

@@ -31,24 +31,12 @@ __device__ __forceinline__ float4 ldg_step(const float *p) {
     return v;
 }
 __device__ __forceinline__ void lean_load_step(LeanConsts &F, const float *p) {
-    const float4 a = ldg_step(p), b = ldg_step(p + 4), c = ldg_step(p + 8), d = ldg_step(p + 12);
-    F.cx = make_float2(a.x, b.x);
-    F.cy = make_float2(a.y, b.y);
-    F.cz = make_float2(a.z, b.z);
-    F.c3 = make_float2(a.w, b.w);
-    F.dx = c.x; F.dy = c.y; F.dz = c.z; F.d3 = c.w;
-    F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
+    lean_from(F, ldg_step(p), ldg_step(p + 4), ldg_step(p + 8), ldg_step(p + 12));
 }
 
 // lean_load from a shared-memory copy of the filter block.
 __device__ __forceinline__ void lean_load_smem(LeanConsts &F, const float4 *q) {
-    const float4 a = q[0], b = q[1], c = q[2], d = q[3];
-    F.cx = make_float2(a.x, b.x);
-    F.cy = make_float2(a.y, b.y);
-    F.cz = make_float2(a.z, b.z);
-    F.c3 = make_float2(a.w, b.w);
-    F.dx = c.x; F.dy = c.y; F.dz = c.z; F.d3 = c.w;
-    F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
+    lean_from(F, q[0], q[1], q[2], q[3]);
 }
 
 // One projected vertex (filter units): P = (X', Y') / d', D = d'.

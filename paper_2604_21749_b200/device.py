@@ -294,8 +294,10 @@ def filter_rows(item_mv: np.ndarray, pos_bound: np.ndarray, p0: float, p1: float
     ed = ef * U * SD * (1 + 2.0 ** -20) + 1e-30
     near_hi = np.maximum(near + 2.0 * ed + 2.0 ** -40 * SD, 4.0 * ed)
     out = np.zeros((n, N.FILTER_FLOATS), dtype=np.float32)
-    out[:, 0:4] = X
-    out[:, 4:8] = Y
+    # (X, Y) rows interleaved: X0 Y0 X1 Y1 X2 Y2 X3 Y3 (filter.cuh: one
+    # 128-bit load gives two FFMA2-ready (X, Y) coefficient pairs)
+    out[:, 0:8:2] = X
+    out[:, 1:8:2] = Y
     out[:, 8:12] = Dd
     out[:, 12] = _f32_up(exy)
     out[:, 13] = _f32_up(ed)

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_s1i_v2" -s 1 -c 1 -o gpurun_out/r12_D_full python tools/frame_once.py D 1 > gpurun_out/r12_ncu_D.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_s1_cull|k_s1_exact" -s 2 -c 2 -o gpurun_out/r12_Bq_full python tools/frame_once.py Bq 1 > gpurun_out/r12_ncu_Bq.log 2>&1
