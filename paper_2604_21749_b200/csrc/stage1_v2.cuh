@@ -184,30 +184,77 @@ __device__ __forceinline__ unsigned strip_bits(const LeanConsts &F, const PV *v,
 // Generic lane (no strip pattern): triangle by triangle, 3 gathers and a
 // per-triangle bound each (lean_bits), so only one triangle's vertices are
 // live at a time.
-__device__ __forceinline__ unsigned generic_bits(const LeanConsts &F,
-                                                 const float4 *__restrict__ pb,
+template <int PF, int IF>
+__device__ __forceinline__ unsigned generic_bits(const LeanConsts &F, const ItemGeo<PF, IF> &G,
                                                  const uint32_t *ix, float W, float H,
                                                  float slack, bool tiny) {
     unsigned bits = 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-        const float4 a = __ldg(pb + ix[3 * t]), b = __ldg(pb + ix[3 * t + 1]),
-                     c = __ldg(pb + ix[3 * t + 2]);
-        const float x[3] = {a.x, b.x, c.x}, y[3] = {a.y, b.y, c.y}, z[3] = {a.z, b.z, c.z};
+        float x[3], y[3], z[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) G.pos32(ix[3 * t + e], x[e], y[e], z[e]);
         const unsigned r = lean_bits(F, x, y, z, W, H, slack, tiny);
         bits |= ((r & 1u) << t) | ((r >> 1) << (4 + t));
     }
     return bits;
 }
 
-// One 48-byte fp64-queue entry: 9 positions + tag (CURAST_QX_WORDS).
-__device__ __forceinline__ void qx_put(const curast_frame_t &f, long long slot, const float3 &a,
-                                       const float3 &b, const float3 &c, long long tag) {
+// A stored vertex: its fp32 position for the filter and, for POS_U16, the raw
+// grid coordinates the queue entry carries (k_s1_exact decodes them in fp64).
+template <int PF>
+struct SV {
+    float3 p;
+};
+template <>
+struct SV<CURAST_POS_U16> {
+    uint2 q;
+};
+
+template <int PF, int IF>
+__device__ __forceinline__ SV<PF> sv_load(const ItemGeo<PF, IF> &G, uint32_t v) {
+    SV<PF> s;
+    if constexpr (PF == CURAST_POS_U16) {
+        s.q = __ldg((const uint2 *)G.pos + v);
+    } else {
+        const float4 q = __ldg((const float4 *)G.pos + v);
+        s.p = make_float3(q.x, q.y, q.z);
+    }
+    return s;
+}
+
+// fp32 position of a stored vertex (POS_U16: ItemGeo::pos32's decode)
+template <int PF, int IF>
+__device__ __forceinline__ float4 sv_pos(const ItemGeo<PF, IF> &G, const SV<PF> &s) {
+    if constexpr (PF == CURAST_POS_U16) {
+        return make_float4(__fmaf_rn(q16_half(s.q.x & 0xFFFFu), G.gs32[0], G.gm32[0]),
+                           __fmaf_rn(q16_half(s.q.x >> 16), G.gs32[1], G.gm32[1]),
+                           __fmaf_rn(q16_half(s.q.y & 0xFFFFu), G.gs32[2], G.gm32[2]), 0.f);
+    } else {
+        return make_float4(s.p.x, s.p.y, s.p.z, 0.f);
+    }
+}
+
+// queue entry payload (words 0-4) of a triangle's three stored vertices
+template <int PF>
+__device__ __forceinline__ void qx_put_sv(const curast_frame_t &f, long long slot,
+                                          const SV<PF> &a, const SV<PF> &b, const SV<PF> &c,
+                                          long long tag) {
     if (slot >= f.qx_cap) return;
     int64_t *e = f.qx + CURAST_QX_WORDS * slot;
-    *(float4 *)e = make_float4(a.x, a.y, a.z, b.x);
-    *(float4 *)(e + 2) = make_float4(b.y, b.z, c.x, c.y);
-    *(float2 *)(e + 4) = make_float2(c.z, 0.0f);
+    if constexpr (PF == CURAST_POS_U16) {
+        // the 9 raw u16 coordinates in words 0-2 (k_s1_exact qx_load_q16)
+        const uint64_t q[9] = {a.q.x & 0xFFFFu, a.q.x >> 16, a.q.y & 0xFFFFu,
+                               b.q.x & 0xFFFFu, b.q.x >> 16, b.q.y & 0xFFFFu,
+                               c.q.x & 0xFFFFu, c.q.x >> 16, c.q.y & 0xFFFFu};
+        *(int4 *)e = make_int4((int)(q[0] | q[1] << 16), (int)(q[2] | q[3] << 16),
+                               (int)(q[4] | q[5] << 16), (int)(q[6] | q[7] << 16));
+        e[2] = (int64_t)q[8];
+    } else {
+        *(float4 *)e = make_float4(a.p.x, a.p.y, a.p.z, b.p.x);
+        *(float4 *)(e + 2) = make_float4(b.p.y, b.p.z, c.p.x, c.p.y);
+        *(float2 *)(e + 4) = make_float2(c.p.z, 0.0f);
+    }
     e[CURAST_QX_TAG] = tag;
 }
 
@@ -250,27 +297,24 @@ __device__ __forceinline__ bool claim_flat(const curast_frame_t &f, int lane, in
 }
 
 // One warp step of k_s1_v2 for a lane pattern KIND (warp-uniform): gather,
-// decide, count, queue the undecided triangles with their positions.  The
-// strip kinds keep their 6 gathered positions for the queue entries.
-template <int KIND>
+// decide, count, queue the undecided triangles with their stored positions.
+// The strip kinds keep their 6 stored vertices for the queue entries.
+template <int KIND, int PF, int IF>
 __device__ __forceinline__ void v2_step(const curast_frame_t &f, const LeanConsts &F,
-                                        const float4 *__restrict__ pb, const uint32_t *ix, int nv,
+                                        const ItemGeo<PF, IF> &G, const uint32_t *ix, int nv,
                                         long long tag, float W, float H, float slack, bool tiny,
                                         unsigned &cnt16, QxReserve &R,
                                         unsigned long long *qcount, int lane, unsigned lt_mask) {
-    float3 p[KIND == 0 ? 1 : 6];
+    SV<PF> sv[KIND == 0 ? 1 : 6];
     unsigned bits;
-    if (KIND == 0) {
-        bits = generic_bits(F, pb, ix, W, H, slack, tiny);
+    if constexpr (KIND == 0) {
+        bits = generic_bits(F, G, ix, W, H, slack, tiny);
     } else {
         PV v[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            const float4 q = __ldg(pb + ix[strip_r(KIND, k)]);
-            p[k] = make_float3(q.x, q.y, q.z);
-        }
+        for (int k = 0; k < 6; ++k) sv[k] = sv_load(G, ix[strip_r(KIND, k)]);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) v[k] = pv_project(F, make_float4(p[k].x, p[k].y, p[k].z, 0.f));
+        for (int k = 0; k < 6; ++k) v[k] = pv_project(F, sv_pos(G, sv[k]));
         bits = strip_bits<KIND>(F, v, W, H, slack, tiny);
     }
     const unsigned vmask = (1u << nv) - 1u;
@@ -291,24 +335,21 @@ __device__ __forceinline__ void v2_step(const curast_frame_t &f, const LeanConst
     for (int t = 0; t < 4; ++t) {
         if ((need >> t) & 1u) {
             const long long slot = qs.at(base + __popc(b[t] & lt_mask));
-            if (KIND == 0) {
-                // generic lanes re-read the positions (L1 hits) instead of
-                // keeping 12 gathered vertices live
-                const float4 va = __ldg(pb + ix[3 * t]), vb = __ldg(pb + ix[3 * t + 1]),
-                             vc = __ldg(pb + ix[3 * t + 2]);
-                qx_put(f, slot, make_float3(va.x, va.y, va.z), make_float3(vb.x, vb.y, vb.z),
-                       make_float3(vc.x, vc.y, vc.z), (tag + t) | flag);
+            if constexpr (KIND == 0) {
+                // generic lanes re-read the stored vertices (L1 hits) instead
+                // of keeping 12 of them live
+                qx_put_sv<PF>(f, slot, sv_load(G, ix[3 * t]), sv_load(G, ix[3 * t + 1]),
+                              sv_load(G, ix[3 * t + 2]), (tag + t) | flag);
             } else {
-                qx_put(f, slot, p[strip_g(KIND, 3 * t)], p[strip_g(KIND, 3 * t + 1)],
-                       p[strip_g(KIND, 3 * t + 2)], (tag + t) | flag);
+                qx_put_sv<PF>(f, slot, sv[strip_g(KIND, 3 * t)], sv[strip_g(KIND, 3 * t + 1)],
+                              sv[strip_g(KIND, 3 * t + 2)], (tag + t) | flag);
             }
         }
         base += __popc(b[t]);
     }
 }
 
-// ------------------------------------------------ filter -> global fp64 queue
-template <int MINB>
+template <int MINB, int PF = CURAST_POS_F32, int IF = CURAST_IDX_U32>
 __global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
     constexpr int STEP = 128;
     const int lane = threadIdx.x & 31;
@@ -333,8 +374,9 @@ __global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
             cnt16 = 0;
         }
         const float *frow = f.item_filter + CURAST_FILTER_FLOATS * item;
-        const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + item);
-        const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + item) + 3 * lo;
+        ItemGeo<PF, IF> G;
+        G.load(f, item);
+        const uint32_t *ib = G.idx + 3 * lo;
         const int n = (int)(hi - lo);
         const bool vec = (((uintptr_t)ib) & 15) == 0;
         const long long tag = (item << 40) | lo;
@@ -346,16 +388,17 @@ __global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
             const int o = s0 + 4 * lane;
             const int nv = max(0, min(4, n - o));
             uint32_t ix[12];
-            load_step_indices(ib, o, nv, vec, ix);
+            if constexpr (IF == CURAST_IDX_U32) load_step_indices(ib, o, nv, vec, ix);
+            else G.template index_run<12>(3 * (lo + o), 3 * nv, ix);   // bit reader
             const int kind = strip_kind(ix, nv == 4);
             if (kind == 1)
-                v2_step<1>(f, F, pb, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
+                v2_step<1>(f, F, G, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
                            lt_mask);
             else if (kind == 2)
-                v2_step<2>(f, F, pb, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
+                v2_step<2>(f, F, G, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
                            lt_mask);
             else
-                v2_step<0>(f, F, pb, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
+                v2_step<0>(f, F, G, ix, nv, tag + o, W, H, slack, tiny, cnt16, R, qcount, lane,
                            lt_mask);
         }
     }
@@ -375,11 +418,11 @@ __global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
 // instance from registers + shared memory — no global load in the instance
 // loop.  Undecided (instance, triangle) pairs go to the fp64 queue with their
 // object-space positions and the instance's item in the tag.
-template <int KIND>
+template <int KIND, int PF, int IF>
 __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (*sF)[4],
                                          const long long *sItem, int ninst,
-                                         const float4 *__restrict__ pb, const uint32_t *ix,
-                                         int nv, long long local0, float W, float H, float slack,
+                                         const ItemGeo<PF, IF> &G, const uint32_t *ix, int nv,
+                                         long long local0, float W, float H, float slack,
                                          bool tiny, unsigned &cnt16, QxReserve &R,
                                          unsigned long long *qcount, int lane,
                                          unsigned lt_mask) {
@@ -388,8 +431,9 @@ __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (
         // generic lanes: triangle by triangle, every instance per triangle
 #pragma unroll 1
         for (int t = 0; t < 4; ++t) {
-            const float4 a = __ldg(pb + ix[3 * t]), b = __ldg(pb + ix[3 * t + 1]),
-                         c = __ldg(pb + ix[3 * t + 2]);
+            const SV<PF> sa = sv_load(G, ix[3 * t]), sb = sv_load(G, ix[3 * t + 1]),
+                         sc = sv_load(G, ix[3 * t + 2]);
+            const float4 a = sv_pos(G, sa), b = sv_pos(G, sb), c = sv_pos(G, sc);
             const float x[3] = {a.x, b.x, c.x}, y[3] = {a.y, b.y, c.y}, z[3] = {a.z, b.z, c.z};
             const bool valid = (vmask >> t) & 1u;
 #pragma unroll 1
@@ -404,26 +448,22 @@ __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (
                 if (bb) {
                     const QxSlots qs = qx_reserve(R, qcount, __popc(bb), lane);
                     if (need)
-                        qx_put(f, qs.at(__popc(bb & lt_mask)), make_float3(a.x, a.y, a.z),
-                               make_float3(b.x, b.y, b.z), make_float3(c.x, c.y, c.z),
-                               (sItem[k] << 40) | (local0 + t));
+                        qx_put_sv<PF>(f, qs.at(__popc(bb & lt_mask)), sa, sb, sc,
+                                      (sItem[k] << 40) | (local0 + t));
                 }
             }
         }
     } else {
-    float3 p[6];
+    SV<PF> sv[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-        const float4 q = __ldg(pb + ix[strip_r(KIND, k)]);
-        p[k] = make_float3(q.x, q.y, q.z);
-    }
+    for (int k = 0; k < 6; ++k) sv[k] = sv_load(G, ix[strip_r(KIND, k)]);
 #pragma unroll 1
     for (int k = 0; k < ninst; ++k) {
         LeanConsts F;
         lean_load_smem(F, sF[k]);
         PV v[6];
 #pragma unroll
-        for (int j = 0; j < 6; ++j) v[j] = pv_project(F, make_float4(p[j].x, p[j].y, p[j].z, 0.f));
+        for (int j = 0; j < 6; ++j) v[j] = pv_project(F, sv_pos(G, sv[j]));
         const unsigned bits = strip_bits<KIND>(F, v, W, H, slack, tiny);
         const unsigned need = bits & vmask, fr = (bits >> 4) & vmask;
         cnt16 += (unsigned)__popc(fr) + ((unsigned)(nv - __popc(need) - __popc(fr)) << 16);
@@ -442,16 +482,16 @@ __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             if ((need >> t) & 1u)
-                qx_put(f, qs.at(base + __popc(b[t] & lt_mask)), p[strip_g(KIND, 3 * t)],
-                       p[strip_g(KIND, 3 * t + 1)], p[strip_g(KIND, 3 * t + 2)],
-                       (tag + t) | flag);
+                qx_put_sv<PF>(f, qs.at(base + __popc(b[t] & lt_mask)), sv[strip_g(KIND, 3 * t)],
+                              sv[strip_g(KIND, 3 * t + 1)], sv[strip_g(KIND, 3 * t + 2)],
+                              (tag + t) | flag);
             base += __popc(b[t]);
         }
     }
     }
 }
 
-template <int MINB>
+template <int MINB, int PF = CURAST_POS_F32, int IF = CURAST_IDX_U32>
 __global__ void __launch_bounds__(256, MINB) k_s1i_v2(const curast_frame_t f) {
     constexpr int STEP = 128;
     __shared__ float4 sF[8][CURAST_INST_BLOCK][4];
@@ -506,25 +546,26 @@ __global__ void __launch_bounds__(256, MINB) k_s1i_v2(const curast_frame_t f) {
                 __ldg((const float4 *)(f.item_filter + CURAST_FILTER_FLOATS * sItem[w][j >> 2]) +
                       (j & 3));
         __syncwarp();
-        const int64_t first = sItem[w][0];
-        const float4 *pb = (const float4 *)f.positions + __ldg(f.item_vtx_off + first);
-        const uint32_t *ib = (const uint32_t *)f.indices + __ldg(f.item_idx_off + first) + 3 * lo;
+        ItemGeo<PF, IF> G;
+        G.load(f, sItem[w][0]);
+        const uint32_t *ib = G.idx + 3 * lo;
         const int n = (int)(hi - lo);
         const bool vec = (((uintptr_t)ib) & 15) == 0;
         for (int s0 = 0; s0 < n; s0 += STEP) {
             const int o = s0 + 4 * lane;
             const int nv = max(0, min(4, n - o));
             uint32_t ix[12];
-            load_step_indices(ib, o, nv, vec, ix);
+            if constexpr (IF == CURAST_IDX_U32) load_step_indices(ib, o, nv, vec, ix);
+            else G.template index_run<12>(3 * (lo + o), 3 * nv, ix);   // bit reader
             const int kind = strip_kind(ix, nv == 4);
             if (kind == 1)
-                v2i_step<1>(f, sF[w], sItem[w], ninst, pb, ix, nv, lo + o, W, H, slack, tiny,
+                v2i_step<1>(f, sF[w], sItem[w], ninst, G, ix, nv, lo + o, W, H, slack, tiny,
                             cnt16, R, qcount, lane, lt_mask);
             else if (kind == 2)
-                v2i_step<2>(f, sF[w], sItem[w], ninst, pb, ix, nv, lo + o, W, H, slack, tiny,
+                v2i_step<2>(f, sF[w], sItem[w], ninst, G, ix, nv, lo + o, W, H, slack, tiny,
                             cnt16, R, qcount, lane, lt_mask);
             else
-                v2i_step<0>(f, sF[w], sItem[w], ninst, pb, ix, nv, lo + o, W, H, slack, tiny,
+                v2i_step<0>(f, sF[w], sItem[w], ninst, G, ix, nv, lo + o, W, H, slack, tiny,
                             cnt16, R, qcount, lane, lt_mask);
         }
     }

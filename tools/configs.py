@@ -42,7 +42,31 @@ def build(name):
     if name == "Dq":
         s, c = gen.config_d()
         return compress_scene(s), c
+    if name == "E200":
+        # config E scaled to one GPU: 200 of its 4,750 displaced grids (800M
+        # triangles, generated in HBM)
+        return gen.config_e(n_meshes=200, on_device=True)
+    if name == "A4":
+        s, c = gen.config_a()
+        return s, cr.Camera(position=c.position, view_transform=c.view_transform, fovy=c.fovy,
+                            aspect=c.aspect, near=c.near, image_width=c.image_width,
+                            image_height=c.image_height, supersampling=4)
     raise ValueError(name)
+
+
+def algorithmic_bytes(pf):
+    """12 B per unique triangle (u32 indices) + 12 B per unique
+    vertex (f32 xyz); compressed: ceil(3 T bits / 8) + 6 B per vertex."""
+    from paper_2604_21749_b200 import _native as N
+    b = 0
+    for m in pf.geo.meshes:
+        T, V = m.triangle_count, m.vertex_count
+        if m.idx_format == N.IDX_PACKED:
+            b += -(-3 * T * m.pack[1] // 8)
+        else:
+            b += 12 * T
+        b += 6 * V if m.pos_format == N.POS_U16 else 12 * V
+    return b
 
 
 def measure(name, steps=20, check=False):
@@ -70,6 +94,8 @@ def measure(name, steps=20, check=False):
         "frame_ms": frame_ms, "tri_per_s": dl.total_triangles / (frame_ms * 1e-3),
         "stage_ms": {"clear": stage[0], "stage1": stage[1], "stage2": stage[2], "stage3": stage[3]},
         "geometry_bytes_resident": geo_bytes,
+        "stage1_algorithmic_bytes": algorithmic_bytes(pf),
+        "stage1_hbm_frac": algorithmic_bytes(pf) / (stage[1] * 1e-3) / 1e9 / 6536.4,
         "pos_format": int(geo.pos_format), "idx_format": int(geo.idx_format),
         "stats": {"s1": vars(st.stage1), "s2": vars(st.stage2), "s3": vars(st.stage3),
                   "exact_fallbacks": st.exact_fallbacks},
