@@ -132,19 +132,42 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workloads
-def e_meshes_default(world: int) -> int:
-    return 4750 if world >= 4 else 1188 * world
+def stage1_bytes(pf, T_rank: int) -> int:
+    """SURVEY §8(d) algorithmic stage-1 bytes of a rank: 12 B per triangle
+    (u32 indices) + 12 B per vertex (f32 xyz) of its shard; compressed
+    storage: ceil(3 T bits / 8) + 6 B per vertex."""
+    from paper_2604_21749_b200 import _native as N
+    V = sum(m.vertex_count for m in pf.geo.meshes)
+    Tm = sum(m.triangle_count for m in pf.geo.meshes)
+    frac = T_rank / max(1, Tm)                 # the part of its meshes this rank reads
+    if pf.geo.idx_format == N.IDX_PACKED:
+        bits = max(m.pack[1] for m in pf.geo.meshes)
+        ib = -(-3 * T_rank * bits // 8)
+    else:
+        ib = 12 * T_rank
+    vb = (6 if pf.geo.pos_format == N.POS_U16 else 12) * V * min(1.0, frac)
+    return int(ib + vb)
 
 
-def build_workload(mode: str, world: int, n: int, e_meshes: int | None):
+def e_meshes_default(world: int, compressed: bool = False) -> int:
+    """The full 4,750-mesh scene where it fits (f32: N >= 4 at 88.6 GB per
+    GPU; compressed: N >= 2 at ~52 GB), else ~89 GB of geometry per GPU."""
+    if world >= 4 or (compressed and world >= 2):
+        return 4750
+    return (2376 if compressed else 1188) * world
+
+
+def build_workload(mode: str, world: int, n: int, e_meshes: int | None,
+                   e_compressed: bool = False):
     """(scene, camera, description, scaling) of a bench mode."""
     from paper_2604_21749_b200 import generators as gen
     from paper_2604_21749_b200.scene import SceneNode
     if mode == "E":
-        m = e_meshes or e_meshes_default(world)
-        scene, cam = gen.config_e(n_meshes=m, on_device=True)
+        m = e_meshes or e_meshes_default(world, e_compressed)
+        scene, cam = gen.config_e(n_meshes=m, on_device=True, compressed=e_compressed)
         return scene, cam, (f"E: {m} distinct displaced n=1414 grids generated in HBM "
-                            f"(SURVEY §8(d)), sort-last over {world} GPU(s)"), "strong"
+                            f"({'u16 positions + 21-bit packed indices' if e_compressed else 'f32 / u32'}"
+                            f", SURVEY §8(d)), sort-last over {world} GPU(s)"), "strong"
     scene, cam = gen.config_b(n=n)
     desc = (f"B: dense grid n={n} (make_tessellated_quad layout) @3840x2160, f32 positions")
     if mode == "B" and world > 1:
@@ -186,7 +209,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     t0 = time.time()
-    scene, cam, desc, scaling = build_workload(args.mode, world, args.n, args.e_meshes)
+    scene, cam, desc, scaling = build_workload(args.mode, world, args.n, args.e_meshes,
+                                               args.e_compressed)
     dl = cr.build_draw_list(scene, cam)
     cfg = cr.RasterConfig(instancing="off")
     total = int(dl.total_triangles)
@@ -259,7 +283,7 @@ def run_ours(args):
     result = None
     if rank == 0:
         hbm, peak_kind = _peaks()
-        s1_bytes = 12 * T_rank + 12 * V_rank
+        s1_bytes = stage1_bytes(pf, T_rank)
         W, H = pf.width, pf.height
         achieved = s1_bytes / (s1_ms * 1e-3) / 1e9
         traffic, traffic_src = None, None
@@ -585,6 +609,8 @@ def main():
     ap.add_argument("--mode", default="B", choices=["B", "strong", "E"])
     ap.add_argument("--n", type=int, default=7071, help="grid tessellation (config B: 7071)")
     ap.add_argument("--e-meshes", type=int, default=None, help="config E meshes (mode E)")
+    ap.add_argument("--e-compressed", action="store_true",
+                    help="mode E with u16 positions + packed indices (19B triangles on 2 GPUs)")
     ap.add_argument("--profile", action="store_true", help="skip e2e / CPU legs (ncu runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

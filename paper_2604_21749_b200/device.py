@@ -68,6 +68,18 @@ class DeviceMesh:
         idx = mesh.indices
         self.triangle_count = int(mesh.triangle_count)
         self.device = device
+        if hasattr(mesh, "generate") and getattr(mesh, "compressed", False):
+            # generated in HBM, stored compressed (config E at 2 GPUs)
+            coords, qgrid, words, pack = mesh.generate_compressed(device)
+            self.pos_format = N.POS_U16
+            self.positions = coords
+            self.vertex_count = int(coords.shape[0])
+            self.qgrid = qgrid
+            self.pos_bound = np.abs(qgrid[:3]) + np.abs(qgrid[3:])
+            self.idx_format = N.IDX_PACKED
+            self.indices = words
+            self.pack = pack
+            return
         if hasattr(mesh, "generate"):
             # generated in HBM (generators.DeviceGeneratedMesh, config E):
             # float32-exact by construction, no host copy

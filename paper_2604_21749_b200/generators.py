@@ -225,13 +225,14 @@ class DeviceGeneratedMesh(Mesh):
     or indices ever exists, so a rank materialises only its shard's meshes
     (SURVEY §7.3 hard part 5).  The bits equal ``displaced_grid(n, seed)``."""
 
-    def __init__(self, n: int, seed: int):
-        super().__init__(positions=("egrid", n, seed), indices=("egrid", n, seed),
-                         triangle_count=2 * n * n,
+    def __init__(self, n: int, seed: int, compressed: bool = False):
+        super().__init__(positions=("egrid", n, seed, compressed),
+                         indices=("egrid", n, seed, compressed), triangle_count=2 * n * n,
                          aabb=np.array([[-0.5, -0.5, E_AABB_Z[0]], [0.5, 0.5, E_AABB_Z[1]]]),
                          name=f"egrid{seed}")
         self.grid_n = n
         self.seed = seed
+        self.compressed = compressed
 
     def vertex_count(self) -> int:
         return (self.grid_n + 1) ** 2
@@ -255,9 +256,42 @@ class DeviceGeneratedMesh(Mesh):
         tri = torch.stack([a, cc, b, b, cc, d], dim=1).reshape(-1).to(torch.int32)
         return pos, tri
 
+    def generate_compressed(self, device):
+        """The same mesh stored as codec.quantize_positions + compress_indices
+        would store it (u16 grid coordinates on the mesh box, indices bit-packed
+        at bit_length(V - 1) bits), built in HBM: (coords int16[V, 4] (x, y, z,
+        0), qgrid float64[6] (grid_min, grid_size), packed int32 words,
+        (min_index, bits))."""
+        import torch
+        pos, tri = self.generate(device)
+        box = torch.from_numpy(np.asarray(self.aabb, dtype=np.float64)).to(device)
+        gmin = box[0]
+        size = box[1] - box[0]
+        size = torch.where(size > 0.0, size, torch.ones_like(size))
+        q = torch.floor(65536.0 * (pos[:, :3].double() - gmin) / size).clamp_(0, 65535)
+        coords = torch.zeros((pos.shape[0], 4), dtype=torch.int32, device=device)
+        coords[:, :3] = q.to(torch.int32)
+        coords = coords.to(torch.int16)                      # u16 bit patterns
+        V = pos.shape[0]
+        b = max(1, int(V - 1).bit_length())
+        n = tri.numel()
+        nwords = (n * b + 31) // 32 + 1
+        words = torch.zeros(nwords + 2, dtype=torch.int64, device=device)
+        rel = tri.to(torch.int64)
+        bit = torch.arange(n, device=device, dtype=torch.int64) * b
+        w, sh = bit >> 5, bit & 31
+        full = rel << sh                                     # < 2^63: fields never overlap
+        words.index_add_(0, w, full & 0xFFFFFFFF)
+        words.index_add_(0, w + 1, full >> 32)
+        packed = words & 0xFFFFFFFF                          # the u32 words, as int32 bits
+        packed = torch.where(packed >= 2 ** 31, packed - 2 ** 32, packed).to(torch.int32)
+        qgrid = np.concatenate([np.asarray(self.aabb[0], dtype=np.float64),
+                                (size.cpu().numpy())])
+        return coords, qgrid, packed, (0, b)
+
 
 def config_e(n_meshes: int = 4750, n: int = 1414, seed: int = 0, width: int = 3840,
-             height: int = 2160, on_device: bool = False):
+             height: int = 2160, on_device: bool = False, compressed: bool = False):
     """E: ~19B unique triangles (4,750 distinct displaced n=1414 grids of
     3,998,792 triangles = 18.99B), tiled edge to edge, overview camera
     @3840x2160.  ``on_device`` makes each mesh a
@@ -271,7 +305,8 @@ def config_e(n_meshes: int = 4750, n: int = 1414, seed: int = 0, width: int = 38
         T = np.eye(4)
         T[0, 3] = c - (cols - 1) / 2.0
         T[1, 3] = r - (rows - 1) / 2.0
-        mesh = DeviceGeneratedMesh(n, seed + k) if on_device else displaced_grid(n, seed + k)
+        mesh = (DeviceGeneratedMesh(n, seed + k, compressed) if on_device
+                else displaced_grid(n, seed + k))
         scene.append(SceneNode(mesh=mesh, transforms=[T]))
     half = max(rows / 2.0, cols / 2.0 * height / width) * 1.02
     dist = half / math.tan(math.radians(30.0))
