@@ -4,7 +4,7 @@ the frame's counters, and whether the words equal the first variant's.
 A variant is "default" or comma-free env assignments joined by '+', e.g.
 CURAST_ILV=1 or CURAST_LIB=/path/to/libcurast_b200.so (an A/B build).
 
-    python tools/s1_ab.py B default:CURAST_ILV=1 [K] [rounds]
+    python tools/s1_ab.py B default:CURAST_INSTANCED_KERNEL=0 [K] [rounds]
 """
 import hashlib
 import json
