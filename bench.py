@@ -203,10 +203,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CURAST_BENCH_SHARED_GPU=1 (harness self-test only): every rank on cuda:0
+    # with a gloo group, so the N>1 code path (shards, composite, max-over-
+    # ranks timing, JSON) runs on a one-GPU box; the numbers are not a
+    # scaling measurement (the ranks share one GPU)
+    shared = os.environ.get("CURAST_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     t0 = time.time()
     scene, cam, desc, scaling = build_workload(args.mode, world, args.n, args.e_meshes,
@@ -266,7 +276,7 @@ def run_ours(args):
     s3_ms = float(np.mean([e[3].elapsed_time(e[4]) for e in evs]))
     clr_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     if world > 1:
-        t = torch.tensor([ms, s1_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, s1_ms], dtype=torch.float64, device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, s1_ms = float(t[0]), float(t[1])
     # k_clear, stage-1 filter, k_s1_exact, k_stage2, k_stage3 (+ the composite)
@@ -323,7 +333,8 @@ def run_ours(args):
                          "unit": "GB/s", "frac": achieved / hbm,
                          "algorithmic_bytes_per_launch": s1_bytes,
                          "algorithmic_bytes": "12 B per triangle (u32 indices) + 12 B per vertex "
-                                              "(f32 xyz) of this rank's shard",
+                                              "(f32 xyz) of this rank's shard; compressed: "
+                                              "ceil(3 T bits / 8) + 6 B per vertex",
                          "traffic": traffic, "traffic_source": traffic_src},
             "clocks": sampler.report(),
             "gpu_launches": launches_per_step * K,
@@ -372,7 +383,8 @@ def e2e_measure(dl, cam, cfg, total, world, rank, steps=5, warmup=3):
         words = call()
     t = (time.perf_counter() - t0) / reps
     if world > 1:
-        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t], dtype=torch.float64,
+                          device="cpu" if dist.get_backend() == "gloo" else "cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt[0])
     from paper_2604_21749_b200.pipeline import _frame_cache
@@ -607,7 +619,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="B", choices=["B", "strong", "E"])
-    ap.add_argument("--n", type=int, default=7071, help="grid tessellation (config B: 7071)")
+    ap.add_argument("--grid-n", dest="n", type=int, default=7071,
+                    help="grid tessellation (config B: 7071)")
     ap.add_argument("--e-meshes", type=int, default=None, help="config E meshes (mode E)")
     ap.add_argument("--e-compressed", action="store_true",
                     help="mode E with u16 positions + packed indices (19B triangles on 2 GPUs)")

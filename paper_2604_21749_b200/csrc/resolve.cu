@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(256, CURAST_RESOLVE_MINB) k_resolve(const cura
             w[k] = v3(x * m[0] + y * m[1] + z * m[2] + m[3], x * m[4] + y * m[5] + z * m[6] + m[7],
                       x * m[8] + y * m[9] + z * m[10] + m[11]);
         }
-        const double xs = (double)(pix % r.width), ys = (double)(r.row0 + pix / r.width);
+        // width * rows < 2^31: 32-bit index arithmetic
+        const int p32 = (int)pix, w32 = (int)r.width;
+        const double xs = (double)(p32 % w32), ys = (double)(r.row0 + p32 / w32);
         const V3 dir = pixel_dir(r, xs, ys);
         const V3 org = v3(r.cam[0], r.cam[1], r.cam[2]);
         // _moller_trumbore_bulk (resolvepass.py:184-205)
@@ -264,7 +266,7 @@ __global__ void k_downsample(const uint8_t *__restrict__ src, int64_t w, int64_t
     const uint32_t *s32 = (const uint32_t *)src;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t ox = p % ow, oy = p / ow;
+        const int ox = (int)p % (int)ow, oy = (int)p / (int)ow;
         uint32_t sum[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int dy = 0; dy < FACTOR; ++dy) {
@@ -462,7 +464,8 @@ extern "C" {
 
 int curast_resolve(const curast_resolve_t *r, void *stream) {
     if (!r || !r->fb || !r->out_rgba || !r->counters || r->width <= 0 || r->height <= 0 ||
-        r->row0 < 0 || r->rows < 0 || r->row0 + r->rows > r->height)
+        r->row0 < 0 || r->rows < 0 || r->row0 + r->rows > r->height ||
+        r->width * r->height >= (1ll << 31))
         return CURAST_E_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     int grid = sms() * 8;

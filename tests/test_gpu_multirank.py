@@ -130,3 +130,28 @@ def test_world2_config_e_scaled_down_shard_local_geometry():
     m0, m1 = set(results["meshes0"]), set(results["meshes1"])
     assert len(m0) < results["n_meshes"] and len(m1) < results["n_meshes"]
     assert len(m0 & m1) <= 1                    # a mesh cut by the shard boundary
+
+
+@pytest.mark.parametrize("mode", ["B", "strong"])
+def test_bench_world2_harness_runs(mode):
+    """bench.py under torchrun at N=2 (both ranks on cuda:0 through the
+    CURAST_BENCH_SHARED_GPU=1 harness self-test switch, gloo composite): the
+    sort-last shards, the composite, the max-over-ranks timing and the one
+    JSON line of rank 0.  Not a scaling measurement."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CURAST_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--mode", mode, "--grid-n", "600", "--profile"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
+    assert d["scaling"] == ("weak" if mode == "B" else "strong")
+    tri = 2 * 600 * 600
+    assert d["config"]["triangles"] == (2 * tri if mode == "B" else tri)
