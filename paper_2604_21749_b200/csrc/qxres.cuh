@@ -57,6 +57,20 @@ __device__ __forceinline__ QxSlots qx_reserve(QxReserve &R, unsigned long long *
     return q;
 }
 
+// tot slots for a step of any size: the reservation blocks for up to
+// CURAST_QX_RES slots, one direct allocation beyond (no holes either way)
+__device__ __forceinline__ QxSlots reserve_slots(QxReserve &R, unsigned long long *qcount,
+                                                 int tot, int lane) {
+    if (tot <= CURAST_QX_RES) return qx_reserve(R, qcount, tot, lane);
+    unsigned base = 0;
+    if (lane == 0) base = (unsigned)atomicAdd(qcount, (unsigned long long)tot);
+    QxSlots q;
+    q.base = __shfl_sync(0xffffffffu, base, 0);
+    q.base2 = 0;
+    q.split = tot;
+    return q;
+}
+
 // the warp's final rest becomes holes
 __device__ __forceinline__ void qx_reserve_close(const curast_frame_t &f, const QxReserve &R, int lane) {
     __syncwarp();

@@ -457,6 +457,11 @@ __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (
     SV<PF> sv[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) sv[k] = sv_load(G, ix[strip_r(KIND, k)]);
+    // the decisions of all instances first (need / frustum bits of
+    // instance k in bits 4k..4k+3, interior flag in bit k), then one
+    // reservation and the queue writes of the whole step
+    unsigned long long needm = 0, frm = 0;
+    unsigned intm = 0;
 #pragma unroll 1
     for (int k = 0; k < ninst; ++k) {
         LeanConsts F;
@@ -465,27 +470,39 @@ __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (
 #pragma unroll
         for (int j = 0; j < 6; ++j) v[j] = pv_project(F, sv_pos(G, sv[j]));
         const unsigned bits = strip_bits<KIND>(F, v, W, H, slack, tiny);
-        const unsigned need = bits & vmask, fr = (bits >> 4) & vmask;
-        cnt16 += (unsigned)__popc(fr) + ((unsigned)(nv - __popc(need) - __popc(fr)) << 16);
-        unsigned b[4];
-        int tot = 0;
+        needm |= (unsigned long long)(bits & vmask) << (4 * k);
+        frm |= (unsigned long long)((bits >> 4) & vmask) << (4 * k);
+        intm |= ((bits >> 8) & 1u) << k;
+    }
+    const int nneed = __popcll(needm), nfr = __popcll(frm);
+    cnt16 += (unsigned)nfr + ((unsigned)(nv * ninst - nneed - nfr) << 16);
+    // warp prefix sum of the per-lane entry counts
+    int incl = nneed;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            b[t] = __ballot_sync(0xffffffffu, (need >> t) & 1u);
-            tot += __popc(b[t]);
-        }
-        if (!tot) continue;
-        const QxSlots qs = qx_reserve(R, qcount, tot, lane);
-        const long long tag = (sItem[k] << 40) | local0;
-        const long long flag = (bits & 0x100u) ? CURAST_QX_INTERIOR : 0ll;
-        int base = 0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            if ((need >> t) & 1u)
-                qx_put_sv<PF>(f, qs.at(base + __popc(b[t] & lt_mask)), sv[strip_g(KIND, 3 * t)],
-                              sv[strip_g(KIND, 3 * t + 1)], sv[strip_g(KIND, 3 * t + 2)],
-                              (tag + t) | flag);
-            base += __popc(b[t]);
+    for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += u;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (!tot) return;
+    const QxSlots qs = reserve_slots(R, qcount, tot, lane);
+    int i = incl - nneed;
+    while (needm) {
+        const int bit = __ffsll((long long)needm) - 1;
+        needm &= needm - 1;
+        const int k = bit >> 2, t = bit & 3;
+        const long long tag = ((sItem[k] << 40) | (local0 + t)) |
+                              (((intm >> k) & 1u) ? CURAST_QX_INTERIOR : 0ll);
+        const long long slot = qs.at(i++);
+        switch (t) {
+        case 0: qx_put_sv<PF>(f, slot, sv[strip_g(KIND, 0)], sv[strip_g(KIND, 1)],
+                              sv[strip_g(KIND, 2)], tag); break;
+        case 1: qx_put_sv<PF>(f, slot, sv[strip_g(KIND, 3)], sv[strip_g(KIND, 4)],
+                              sv[strip_g(KIND, 5)], tag); break;
+        case 2: qx_put_sv<PF>(f, slot, sv[strip_g(KIND, 6)], sv[strip_g(KIND, 7)],
+                              sv[strip_g(KIND, 8)], tag); break;
+        default: qx_put_sv<PF>(f, slot, sv[strip_g(KIND, 9)], sv[strip_g(KIND, 10)],
+                               sv[strip_g(KIND, 11)], tag); break;
         }
     }
     }
