@@ -236,3 +236,51 @@ def test_div_shared_equals_ieee_division(mode):
     assert bad == 0 and rbad == 0, (checked, bad, slow, rbad)
     if mode == 1:
         assert slow == 0          # the rasterizer's magnitudes never leave the fast path
+
+
+def _vs_oracle(scene, cam, cfg=None):
+    cfg = cfg or RasterConfig()
+    dl = build_draw_list(scene, cam)
+    fb, st = render_draw_list(dl, cam, cfg)
+    ref, rst, _ = oh.render_reference(scene, cam, tiny_cull=cfg.tiny_cull,
+                                      force_stage=cfg.force_stage)
+    assert np.array_equal(fb.words, ref)
+    if rst is not None:
+        assert np.array_equal(stats_vector_from_frame(st), stats_vector_from_oracle(rst))
+    return fb, st
+
+
+def test_edge_cases_empty_behind_degenerate_tiny_frames():
+    """Edge cases of kernels.py:49-157 through the GPU path: a scene whose
+    every triangle is behind the camera (all CULL_FRUSTUM after the draw
+    list keeps the node), collinear (degenerate) and zero-area triangles,
+    1x1 / 3x2 / 1x64 frames, a frame with no surviving item (CLEAR, empty
+    stats), and single-triangle meshes at unaligned index offsets."""
+    cam = identity_camera(width=64, height=48)
+    # every vertex behind the camera; the node's box straddles the near
+    # plane so the draw list keeps it
+    p = np.array([[0, 0, 1.0], [0.1, 0, 1.0], [0, 0.1, 1.0],
+                  [-1, -1, -5.0], [1, -1, -5.0], [0, 1, 0.5]], dtype=np.float64)
+    m = mesh_from_soup(p)
+    _vs_oracle([SceneNode(mesh=m, transforms=[np.eye(4)])], cam)
+    # degenerate: collinear and repeated vertices, in front of the camera
+    pix = [(10.25, 10.25), (20.25, 20.25), (30.25, 30.25)]
+    deg = pixel_triangle_scene(pix, [2.0, 2.0, 2.0], cam)
+    pix2 = [(5.5, 5.5), (5.5, 5.5), (9.5, 7.5)]
+    deg += pixel_triangle_scene(pix2, [3.0, 3.0, 3.0], cam)
+    fb, st = _vs_oracle(deg, cam)
+    assert st.stage1.culled_degenerate + st.stage1.culled_offscreen + st.stage1.culled_tiny > 0
+    # tiny frames
+    rng = np.random.default_rng(9)
+    for w, h in ((1, 1), (3, 2), (1, 64)):
+        scene, _ = random_scene(rng)
+        c = Camera.look_at((0.0, 0.0, 6.0), (0.0, 0.0, 0.0), width=w, height=h)
+        dl = build_draw_list(scene, c)
+        if dl.total_triangles:
+            _vs_oracle(scene, c)
+    # nothing survives the draw-list cull: a CLEAR frame
+    c = Camera.look_at((0.0, 0.0, 6.0), (0.0, 0.0, 12.0), width=32, height=16)
+    scene = [SceneNode(mesh=m, transforms=[np.eye(4)])]
+    dl = build_draw_list(scene, c)
+    fb, st = render_draw_list(dl, c)
+    assert dl.total_triangles == 0 and (fb.words == CLEAR).all() and st.fragments == 0
