@@ -120,33 +120,4 @@ __device__ __forceinline__ void lean_load(LeanConsts &F, const float *__restrict
     lean_from(F, __ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(q + 3));
 }
 
-// Projected triangle: P[k] = (px', py') with |px' - px64| <= eps per
-// coordinate (error model above), dmin = min d', bbox of the P[k].
-struct LeanTri {
-    float2 P[3];
-    float dmin, mnx, mxx, mny, mxy, eps;
-};
-
-__device__ __forceinline__ void lean_project(LeanTri &T, const LeanConsts &F, const float *x,
-                                             const float *y, const float *z, float slack) {
-    float D[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        D[k] = __fmaf_rn(F.dz, z[k], __fmaf_rn(F.dy, y[k], __fmaf_rn(F.dx, x[k], F.d3)));
-        float2 t = __ffma2_rn(F.cx, make_float2(x[k], x[k]), F.c3);
-        t = __ffma2_rn(F.cy, make_float2(y[k], y[k]), t);
-        t = __ffma2_rn(F.cz, make_float2(z[k], z[k]), t);
-        const float r = rcp_approx(D[k]);
-        T.P[k] = __fmul2_rn(t, make_float2(r, r));
-    }
-    T.dmin = fminf(D[0], fminf(D[1], D[2]));
-    T.mnx = fminf(T.P[0].x, fminf(T.P[1].x, T.P[2].x));
-    T.mxx = fmaxf(T.P[0].x, fmaxf(T.P[1].x, T.P[2].x));
-    T.mny = fminf(T.P[0].y, fminf(T.P[1].y, T.P[2].y));
-    T.mxy = fmaxf(T.P[0].y, fmaxf(T.P[1].y, T.P[2].y));
-    const float M = fmaxf(fmaxf(fabsf(T.mnx), fabsf(T.mxx)), fmaxf(fabsf(T.mny), fabsf(T.mxy)));
-    const float e = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(T.dmin);
-    T.eps = __fmaf_rn(e, 1.5f, __fmaf_rn(M, kRelSlack, slack));
-}
-
 }  // namespace curast

@@ -33,49 +33,6 @@ __device__ __forceinline__ void load_filter_pairs(FilterPairs &F, const float *_
     F.exy = d.x; F.ed = d.y; F.near_hi = d.z;
 }
 
-// fp32 cull filter on one triangle with packed (x, y) arithmetic.  Same
-// decisions and bound as filter_tri (filter.cuh).
-__device__ __forceinline__ int filter_tri2(const FilterPairs &F, const float *vx, const float *vy,
-                                           const float *vz, float2 WH, float slack, bool tiny_cull) {
-    float2 P[3];
-    float D[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        float2 t = __ffma2_rn(F.cx, make_float2(vx[k], vx[k]), F.c3);
-        t = __ffma2_rn(F.cy, make_float2(vy[k], vy[k]), t);
-        t = __ffma2_rn(F.cz, make_float2(vz[k], vz[k]), t);
-        D[k] = __fmaf_rn(F.dz, vz[k], __fmaf_rn(F.dy, vy[k], __fmaf_rn(F.dx, vx[k], F.d3)));
-        float r = rcp_approx(D[k]);
-        P[k] = __fmul2_rn(t, make_float2(r, r));
-    }
-    const float dmin = fminf(D[0], fminf(D[1], D[2]));
-    if (!(dmin > F.near_hi)) return FILT_EXACT;          // near-plane outcomes: exact
-    const float2 mn = make_float2(fminf(P[0].x, fminf(P[1].x, P[2].x)),
-                                  fminf(P[0].y, fminf(P[1].y, P[2].y)));
-    const float2 mx = make_float2(fmaxf(P[0].x, fmaxf(P[1].x, P[2].x)),
-                                  fmaxf(P[0].y, fmaxf(P[1].y, P[2].y)));
-    const float M = fmaxf(fmaxf(fabsf(mn.x), fabsf(mx.x)), fmaxf(fabsf(mn.y), fabsf(mx.y)));
-    float eps = __fmaf_rn(M, F.ed, F.exy) * rcp_approx(dmin);
-    eps = __fmaf_rn(eps, 1.5f, __fmaf_rn(M, kRelSlack, slack));
-    const float2 e2 = make_float2(eps, eps);
-    const float2 lo = __fadd2_rn(mn, make_float2(-eps, -eps));   // min - eps
-    const float2 hi = __fadd2_rn(mx, e2);                       // max + eps
-    // NDC frustum (kernels.py:85-89): all px < 0 | all px > W | py likewise
-    const float2 lo_w = __fadd2_rn(lo, make_float2(-WH.x, -WH.y));
-    if (fminf(hi.x, hi.y) < 0.0f || fmaxf(lo_w.x, lo_w.y) > 0.0f) return CULL_FRUSTUM;
-    if (!tiny_cull) return FILT_EXACT;
-    const float2 mxl = __fadd2_rn(mx, make_float2(-eps, -eps));  // max - eps
-    const float2 mnh = __fadd2_rn(mn, __fadd2_rn(e2, make_float2(-WH.x, -WH.y)));  // min + eps - WH
-    const float2 ext = __fadd2_rn(mxl, make_float2(-mn.x - eps, -mn.y - eps));      // max-min-2eps
-    // provably not frustum-culled, not offscreen (kernels.py:98-108)
-    const bool decided = fminf(mxl.x, mxl.y) > 0.0f && fmaxf(mnh.x, mnh.y) < 0.0f &&
-                         fminf(ext.x, ext.y) > 0.0f;
-    // tiny (kernels.py:110-115): smallest sample centre >= min lies > max
-    const float2 h = __fadd2_rn(make_float2(ceilf(lo.x - 0.5f), ceilf(lo.y - 0.5f)),
-                                make_float2(0.5f, 0.5f));
-    if (decided && (h.x > hi.x || h.y > hi.y)) return CULL_TINY;
-    return FILT_EXACT;
-}
 
 // Scalar fp32 cull filter, same decisions and bound as filter_tri, with a
 // short path for triangles whose eps-expanded bbox lies strictly inside the

@@ -74,15 +74,4 @@ __device__ __forceinline__ unsigned lean_bits(const LeanConsts &F, const float *
                        lean_vertex(F, x[2], y[2], z[2]), W, H, slack, tiny);
 }
 
-// fp64 queue entry: the 9 object-space positions + tag (CURAST_QX_WORDS)
-__device__ __forceinline__ void qx_write(const curast_frame_t &f, long long slot, const float *x,
-                                         const float *y, const float *z, long long tag) {
-    if (slot >= f.qx_cap) return;
-    int64_t *e = f.qx + CURAST_QX_WORDS * slot;
-    *(float4 *)e = make_float4(x[0], y[0], z[0], x[1]);
-    *(float4 *)(e + 2) = make_float4(y[1], z[1], x[2], y[2]);
-    *(float2 *)(e + 4) = make_float2(z[2], 0.0f);
-    e[CURAST_QX_TAG] = tag;
-}
-
 }  // namespace curast
