@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+python tools/s1_ab.py C default:CURAST_LIB=tools/ab/base.so 20 3 > gpurun_out/late30_ab_C.jsonl 2>&1
+python tools/s1_ab.py A default:CURAST_LIB=tools/ab/base.so 20 2 > gpurun_out/late30_ab_A.jsonl 2>&1

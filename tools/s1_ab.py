@@ -41,7 +41,8 @@ def child(config, K):
     h = hashlib.sha256(pf.fb.cpu().numpy().tobytes()).hexdigest()[:16]
     from scenes import stats_vector_from_frame
     sv = stats_vector_from_frame(pf.stats(c, [0] * 4)).tolist()
-    print(json.dumps({"frame_ms": fr, "stage1_ms": float(st[1]), "words": h, "stats": sv}))
+    print(json.dumps({"frame_ms": fr, "stage1_ms": float(st[1]), "stage2_ms": float(st[2]),
+                      "stage3_ms": float(st[3]), "words": h, "stats": sv}))
 
 
 if __name__ == "__main__":
