@@ -117,7 +117,8 @@ typedef struct curast_frame {
     const int64_t *item_pack;         /* PACKED: int64[n_items][2] min, bits  */
     /* ---- instancing groups (pipeline.py:114-135) ---- */
     int32_t instanced;                /* 1: stage1_instanced_range semantics  */
-    int32_t use_filter;               /* 1: fp32 cull filter + fp64 fallback  */
+    int32_t use_filter;               /* 1: fp32 cull filter + fp64 fallback
+                                         (ignored when force_stage >= 2)      */
     int64_t n_groups;
     const int64_t *group_prefix;      /* int64[n_groups+1] unique triangles   */
     const int64_t *group_item_off;

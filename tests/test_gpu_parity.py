@@ -284,3 +284,25 @@ def test_edge_cases_empty_behind_degenerate_tiny_frames():
     dl = build_draw_list(scene, c)
     fb, st = render_draw_list(dl, c)
     assert dl.total_triangles == 0 and (fb.words == CLEAR).all() and st.fragments == 0
+
+
+@pytest.mark.parametrize("force", [2, 3])
+def test_abi_filter_flag_ignored_when_forcing_stages(force):
+    """force_stage >= 2 forwards every triangle before the frustum and tiny
+    tests (kernels.py:73-76), so the fp32 cull filter must not decide: a C-ABI
+    caller that leaves frame.use_filter = 1 still gets the reference's words
+    and counters (the library drops the filter itself)."""
+    from paper_2604_21749_b200.pipeline import PreparedFrame
+    rng = np.random.default_rng(11 + force)
+    for _ in range(3):
+        scene, cam = random_scene(rng)
+        cfg = RasterConfig(force_stage=force)
+        dl = build_draw_list(scene, cam)
+        pf = PreparedFrame(dl, cam, cfg)
+        pf.frame.use_filter = 1
+        c, secs = pf.run()
+        ref, rst, _ = oh.render_reference(scene, cam, force_stage=force)
+        assert np.array_equal(pf.fb.cpu().numpy().view(np.uint64), ref)
+        if rst is not None:
+            assert np.array_equal(stats_vector_from_frame(pf.stats(c, secs)),
+                                  stats_vector_from_oracle(rst))

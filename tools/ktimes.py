@@ -1,0 +1,38 @@
+"""Per-kernel device times (torch.profiler / CUPTI) of one config's frame,
+and its exact-fallback count: python tools/ktimes.py <config> [frames]"""
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import paper_2604_21749_b200 as cr  # noqa: E402
+from paper_2604_21749_b200.pipeline import PreparedFrame  # noqa: E402
+from frame_once import scene_for  # noqa: E402
+
+name = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+scene, cam = scene_for(name)
+dl = cr.build_draw_list(scene, cam)
+pf = PreparedFrame(dl, cam, cr.RasterConfig(), fresh_fb=False)
+c, _ = pf.run()
+st = pf.stats(pf.read_counters(), [0] * 4)
+for _ in range(3):
+    pf.launch()
+torch.cuda.synchronize()
+from torch.profiler import profile, ProfilerActivity  # noqa: E402
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(n):
+        pf.launch()
+    torch.cuda.synchronize()
+ker = {}
+for ev in prof.key_averages():
+    if ev.device_time_total > 0:
+        ker[ev.key[:60]] = round(ev.device_time_total / max(1, ev.count) / 1000.0, 4)
+print(json.dumps({"config": name, "env": {k: v for k, v in os.environ.items()
+                                          if k.startswith("CURAST_")},
+                  "exact_fallbacks": st.exact_fallbacks, "kernels_ms": ker}))
