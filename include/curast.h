@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CURAST_ABI_VERSION 2
+#define CURAST_ABI_VERSION 3
 
 enum curast_pos_format {
     CURAST_POS_F64 = 0,   /* double[V][3] (reference ctx.positions)            */
@@ -155,6 +155,13 @@ typedef struct curast_frame {
     /* ---- config (config.py:11-22) ---- */
     int32_t tiny_cull;
     int32_t force_stage;
+    int32_t s1_row_raster;            /* 1: the fp64 pass hands stage-1 raster
+                                         bboxes of >= 16 pixels and 2 rows to
+                                         its whole warp (one row per lane; same
+                                         operations): for frames of larger
+                                         triangles (host: >= 1 stage-1 fragment
+                                         per rasterized triangle)             */
+    int32_t reserved0;
     int64_t small_max, medium_max, tile_px;
     /* ---- outputs (device pointers) ---- */
     uint64_t *fb;                     /* uint64[width*height]                 */

@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CURAST_LIB") or os.path.join(_HERE, "libcurast_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 POS_F64, POS_F32, POS_U16 = 0, 1, 2
 IDX_U32, IDX_PACKED = 0, 1
@@ -52,7 +52,7 @@ class CurastFrame(ctypes.Structure):
         ("inst_unit_hi", _P), ("inst_unit_chunk_prefix", _P), ("inst_chunk_tris", _I64),
         ("p0", _D), ("p1", _D), ("near", _D), ("width", _I64), ("height", _I64),
         ("rot_t", _D * 9), ("cam", _D * 3), ("view_r2", _D * 3), ("view_t2", _D),
-        ("tiny_cull", _I32), ("force_stage", _I32),
+        ("tiny_cull", _I32), ("force_stage", _I32), ("s1_row_raster", _I32), ("reserved0", _I32),
         ("small_max", _I64), ("medium_max", _I64), ("tile_px", _I64),
         ("fb", _P), ("q2", _P), ("q2_cap", _I64), ("q3", _P), ("q3_cap", _I64),
         ("qx", _P), ("qx_cap", _I64), ("counters", _P),

@@ -437,6 +437,7 @@ class PreparedFrame:
         f.view_t2 = float(view[2, 3])
         f.tiny_cull = int(bool(cfg.tiny_cull))
         f.force_stage = int(cfg.force_stage)
+        f.s1_row_raster = 0
         f.small_max = int(cfg.small_max_px)
         f.medium_max = int(cfg.medium_max_px)
         f.tile_px = int(cfg.tile_px)
@@ -553,6 +554,16 @@ class PreparedFrame:
         writes into this frame's previous, still-referenced buffers)."""
         return getattr(self, "_graph_queues", None) is not self._queues
 
+    def _choose_row_raster(self, c) -> None:
+        """Frames whose stage-1 triangles average at least one fragment
+        (larger triangles: config C 1.3, A4) let the fp64 pass rasterize wide
+        bboxes row-parallel (curast.h s1_row_raster); dense frames (B 0.5,
+        D 0.3) keep the per-thread loop, which the extra per-entry check would
+        slow by ~2%.  Same words and counters either way; applies from the
+        next launch (re-capture a graph taken before)."""
+        rast, frags = int(c[N.C_S1 + 0]), int(c[N.C_S1 + 7])
+        self.frame.s1_row_raster = int(rast > 0 and frags >= rast)
+
     def read_counters(self) -> np.ndarray:
         ws = self.ws
         ws.counters_host.copy_(ws.counters, non_blocking=True)
@@ -589,6 +600,7 @@ class PreparedFrame:
             secs = [0.0] * 4
             if timed:
                 secs = [events[i].elapsed_time(events[i + 1]) * 1e-3 for i in range(4)]
+            self._choose_row_raster(c)
             return c, secs
 
     def stats(self, c: np.ndarray, secs) -> FrameStats:

@@ -306,3 +306,36 @@ def test_abi_filter_flag_ignored_when_forcing_stages(force):
         if rst is not None:
             assert np.array_equal(stats_vector_from_frame(pf.stats(c, secs)),
                                   stats_vector_from_oracle(rst))
+
+
+@pytest.mark.parametrize("force", [0, 1])
+def test_row_parallel_stage1_raster_matches_oracle(force):
+    """frame.s1_row_raster = 1: the fp64 pass hands stage-1 bboxes of >= 16
+    pixels / 2 rows to its warp (one row per lane, the row's serial s/t
+    stepping kept, kernels.py:140-157).  Random scenes and, with force_stage 1
+    (every triangle rasterized in stage 1, so large bboxes overflow the four
+    per-warp slots into the thread's own loop), the same words and counters
+    as the oracle."""
+    from paper_2604_21749_b200 import _native as N
+    from paper_2604_21749_b200.pipeline import PreparedFrame
+    rng = np.random.default_rng(21 + force)
+    cases = [random_scene(rng) for _ in range(4)]
+    cases.append(gen.config_c(width=640, height=360))
+    for scene, cam in cases:
+        cfg = RasterConfig(force_stage=force)
+        dl = build_draw_list(scene, cam)
+        pf = PreparedFrame(dl, cam, cfg)
+        pf.frame.s1_row_raster = 1
+        pf.launch()
+        c = pf.read_counters()
+        if int(c[N.C_QX]) > pf.qx_alloc or int(c[0]) > pf.q2_alloc or int(c[1]) > pf.q3_alloc:
+            pf.run()                      # sized the queues (resets the flag)
+            pf.frame.s1_row_raster = 1
+            pf.launch()
+            c = pf.read_counters()
+        ref, rst, _ = oh.render_reference(scene, cam, force_stage=force)
+        assert np.array_equal(pf.fb.cpu().numpy().view(np.uint64), ref)
+        if rst is not None:
+            assert np.array_equal(stats_vector_from_frame(pf.stats(c, [0.0] * 4)),
+                                  stats_vector_from_oracle(rst))
+
