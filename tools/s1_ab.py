@@ -28,6 +28,8 @@ def child(config, K):
     dl = cr.build_draw_list(scene, cam)
     pf = PreparedFrame(dl, cam, cr.RasterConfig(), fresh_fb=False)
     c, _ = pf.run()
+    if os.environ.get("AB_ROW_RASTER") is not None:      # override the host's choice
+        pf.frame.s1_row_raster = int(os.environ["AB_ROW_RASTER"])
     for _ in range(3):
         pf.launch()
     torch.cuda.synchronize()
