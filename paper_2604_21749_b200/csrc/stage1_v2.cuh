@@ -93,6 +93,7 @@ __device__ __forceinline__ LaneB lane_bound(const LeanConsts &F, const PV *v, fl
 
 // Tiny-cull decision of an interior triangle (every frustum / near /
 // offscreen outcome provably false except a zero extent): 1 = fp64 needed.
+template <bool FLAT_LOGIC = false>
 __device__ __forceinline__ unsigned tri_fast(const PV &a, const PV &b, const PV &c, const LaneB &L,
                                              bool tiny) {
     const float mnx = fminf(a.P.x, fminf(b.P.x, c.P.x)), mxx = fmaxf(a.P.x, fmaxf(b.P.x, c.P.x));
@@ -100,9 +101,18 @@ __device__ __forceinline__ unsigned tri_fast(const PV &a, const PV &b, const PV 
     const float2 ext = __fadd2_rn(make_float2(mxx, mxy), make_float2(-mnx, -mny));
     const float2 lo = __fadd2_rn(make_float2(mnx, mny), make_float2(-L.lo5, -L.lo5));
     const float2 hi = __fadd2_rn(make_float2(mxx, mxy), make_float2(L.hi5, L.hi5));
-    const bool e = (ext.x > L.e2) && (ext.y > L.e2);
-    const bool t = (ceilf(lo.x) > hi.x) || (ceilf(lo.y) > hi.y);
-    return (tiny && e && t) ? 0u : 1u;
+    if constexpr (FLAT_LOGIC) {
+        // non-short-circuit predicate logic: fewer selects (instanced kernel,
+        // issue-bound: D 3.11 -> 3.05 ms); the streamed kernel keeps the
+        // short-circuit form, whose predicated ceil is off its load chain
+        const bool e = (ext.x > L.e2) & (ext.y > L.e2);
+        const bool t = (ceilf(lo.x) > hi.x) | (ceilf(lo.y) > hi.y);
+        return (tiny & e & t) ? 0u : 1u;
+    } else {
+        const bool e = (ext.x > L.e2) && (ext.y > L.e2);
+        const bool t = (ceilf(lo.x) > hi.x) || (ceilf(lo.y) > hi.y);
+        return (tiny && e && t) ? 0u : 1u;
+    }
 }
 
 // Full decision (lean_decide) under the lane bound: bit 0 fp64, bit 1 frustum.
@@ -160,7 +170,7 @@ static_assert(strip_r(1, 3) == 5 && strip_r(1, 5) == 11 && strip_r(2, 3) == 4 &&
 // vertices under one lane bound: need bits in bits 0-3, frustum bits in bits
 // 4-7, bit 8 = the lane's vertices are provably in front of the near plane
 // and inside the viewport (CURAST_QX_INTERIOR for its queue entries).
-template <int KIND>
+template <int KIND, bool FLAT_LOGIC = false>
 __device__ __forceinline__ unsigned strip_bits(const LeanConsts &F, const PV *v, float W, float H,
                                                float slack, bool tiny) {
     const LaneB L = lane_bound<6>(F, v, W, H, slack);
@@ -168,8 +178,8 @@ __device__ __forceinline__ unsigned strip_bits(const LeanConsts &F, const PV *v,
     if (__all_sync(0xffffffffu, L.interior)) {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            bits |= tri_fast(v[strip_g(KIND, 3 * t)], v[strip_g(KIND, 3 * t + 1)],
-                             v[strip_g(KIND, 3 * t + 2)], L, tiny) << t;
+            bits |= tri_fast<FLAT_LOGIC>(v[strip_g(KIND, 3 * t)], v[strip_g(KIND, 3 * t + 1)],
+                                         v[strip_g(KIND, 3 * t + 2)], L, tiny) << t;
     } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -483,7 +493,7 @@ __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (
         PV v[6];
 #pragma unroll
         for (int j = 0; j < 6; ++j) v[j] = pv_project(F, sv_pos(G, sv[j]));
-        const unsigned bits = strip_bits<KIND>(F, v, W, H, slack, tiny);
+        const unsigned bits = strip_bits<KIND, true>(F, v, W, H, slack, tiny);
         needm |= (unsigned long long)(bits & vmask) << (4 * k);
         frm |= (unsigned long long)((bits >> 4) & vmask) << (4 * k);
         intm |= ((bits >> 8) & 1u) << k;
