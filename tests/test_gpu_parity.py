@@ -308,8 +308,8 @@ def test_abi_filter_flag_ignored_when_forcing_stages(force):
                                   stats_vector_from_oracle(rst))
 
 
-@pytest.mark.parametrize("force", [0, 1])
-def test_row_parallel_stage1_raster_matches_oracle(force):
+@pytest.mark.parametrize("force,compressed", [(0, False), (1, False), (0, True), (1, True)])
+def test_row_parallel_stage1_raster_matches_oracle(force, compressed):
     """frame.s1_row_raster = 1: the fp64 pass hands stage-1 bboxes of >= 16
     pixels / 2 rows to its warp (one row per lane, the row's serial s/t
     stepping kept, kernels.py:140-157).  Random scenes and, with force_stage 1
@@ -321,6 +321,10 @@ def test_row_parallel_stage1_raster_matches_oracle(force):
     rng = np.random.default_rng(21 + force)
     cases = [random_scene(rng) for _ in range(4)]
     cases.append(gen.config_c(width=640, height=360))
+    if compressed:
+        # u16 grid positions + packed indices: the fp64 pass's u16 queue entries
+        from scenes import compress_scene
+        cases = [(compress_scene(sc), cam) for sc, cam in cases]
     for scene, cam in cases:
         cfg = RasterConfig(force_stage=force)
         dl = build_draw_list(scene, cam)
