@@ -405,3 +405,25 @@ def test_benchcli_rows_mirror_the_reference_toggles(tmp_path):
     benchcli.write_csv(rep, out)
     assert out.read_text().splitlines()[0] == ",".join(benchcli.COLS)
     assert "stage1Ms" in benchcli.format_table(rep).splitlines()[0]
+
+
+def test_row_raster_choice_follows_fragments_per_triangle():
+    """PreparedFrame._choose_row_raster: the fp64 pass's row-parallel raster
+    (curast.h s1_row_raster) only for frames averaging >= 1 stage-1 fragment
+    per rasterized triangle — config C (604,610 / 462,315) and A4 on, the
+    dense configs B (4,666,508 / 9,331,200) and D (0.32) off, empty frames off."""
+    import types
+    from paper_2604_21749_b200 import _native as N
+    from paper_2604_21749_b200.pipeline import PreparedFrame
+
+    def choose(rast, frags):
+        c = np.zeros(N.COUNTER_SLOTS, dtype=np.int64)
+        c[N.C_S1 + 0], c[N.C_S1 + 7] = rast, frags
+        pf = types.SimpleNamespace(frame=N.CurastFrame())
+        PreparedFrame._choose_row_raster(pf, c)
+        return pf.frame.s1_row_raster
+
+    assert choose(462_315, 604_610) == 1
+    assert choose(9_331_200, 4_666_508) == 0
+    assert choose(7_097_009, 2_276_079) == 0
+    assert choose(0, 0) == 0
