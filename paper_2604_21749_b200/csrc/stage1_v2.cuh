@@ -21,6 +21,7 @@
 #include "filter.cuh"
 #include "qxres.cuh"
 
+
 namespace curast {
 
 // lean_load through volatile non-coherent loads (kept inside the step loop).
@@ -257,24 +258,41 @@ __device__ __forceinline__ void qx_put_sv(const curast_frame_t &f, long long slo
         const uint64_t q[9] = {a.q.x & 0xFFFFu, a.q.x >> 16, a.q.y & 0xFFFFu,
                                b.q.x & 0xFFFFu, b.q.x >> 16, b.q.y & 0xFFFFu,
                                c.q.x & 0xFFFFu, c.q.x >> 16, c.q.y & 0xFFFFu};
-        *(int4 *)e = make_int4((int)(q[0] | q[1] << 16), (int)(q[2] | q[3] << 16),
-                               (int)(q[4] | q[5] << 16), (int)(q[6] | q[7] << 16));
-        e[2] = (int64_t)q[8];
+        __stcs((int4 *)e, make_int4((int)(q[0] | q[1] << 16), (int)(q[2] | q[3] << 16),
+                                    (int)(q[4] | q[5] << 16), (int)(q[6] | q[7] << 16)));
+        __stcs((long long *)(e + 2), (long long)q[8]);
+        __stcs((long long *)(e + CURAST_QX_TAG), tag);
+        return;
     } else {
-        *(float4 *)e = make_float4(a.p.x, a.p.y, a.p.z, b.p.x);
-        *(float4 *)(e + 2) = make_float4(b.p.y, b.p.z, c.p.x, c.p.y);
-        *(float2 *)(e + 4) = make_float2(c.p.z, 0.0f);
+        // streaming stores (evict-first): the queue is read once, by the
+        // fp64 pass, and should not displace the vertex rows L2 holds for
+        // the next grid row's chunk (with the index stream's streaming loads:
+        // B 0.668 -> 0.661 ms stage 1, E200 3.97 -> 3.68 ms)
+        __stcs((float4 *)e, make_float4(a.p.x, a.p.y, a.p.z, b.p.x));
+        __stcs((float4 *)(e + 2), make_float4(b.p.y, b.p.z, c.p.x, c.p.y));
+        __stcs((float2 *)(e + 4), make_float2(c.p.z, 0.0f));
+        __stcs((long long *)(e + CURAST_QX_TAG), tag);
+        return;
     }
     e[CURAST_QX_TAG] = tag;
 }
 
 // The warp's 128-triangle step at chunk offset s0: indices of triangles
 // o .. o+3 (o = s0 + 4 lane) into ix[12]; nv valid triangles.
+// STREAM: the flat table reads each index once per frame — streaming
+// (evict-first) loads; the instanced kernel re-reads a group's run for every
+// instance block and keeps the default policy.
+template <bool STREAM = false>
 __device__ __forceinline__ void load_step_indices(const uint32_t *__restrict__ ib, int o, int nv,
                                                   bool vec, uint32_t *ix) {
     if (vec && nv == 4) {
         const uint4 *v = (const uint4 *)(ib + 3 * o);
-        const uint4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
+        uint4 a, b, d;
+        if constexpr (STREAM) {
+            a = __ldcs(v); b = __ldcs(v + 1); d = __ldcs(v + 2);
+        } else {
+            a = __ldg(v); b = __ldg(v + 1); d = __ldg(v + 2);
+        }
         ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w;
         ix[4] = b.x; ix[5] = b.y; ix[6] = b.z; ix[7] = b.w;
         ix[8] = d.x; ix[9] = d.y; ix[10] = d.z; ix[11] = d.w;
@@ -398,7 +416,7 @@ __global__ void __launch_bounds__(256, MINB) k_s1_v2(const curast_frame_t f) {
             const int o = s0 + 4 * lane;
             const int nv = max(0, min(4, n - o));
             uint32_t ix[12];
-            if constexpr (IF == CURAST_IDX_U32) load_step_indices(ib, o, nv, vec, ix);
+            if constexpr (IF == CURAST_IDX_U32) load_step_indices<true>(ib, o, nv, vec, ix);
             else G.template index_run<12>(3 * (lo + o), 3 * nv, ix);   // bit reader
             if constexpr (IF == CURAST_IDX_U32) {
                 // L2 prefetch of the next step's index lines (12 x 128 B,
