@@ -22,6 +22,7 @@
 #include "qxres.cuh"
 
 
+
 namespace curast {
 
 // lean_load through volatile non-coherent loads (kept inside the step loop).
@@ -222,11 +223,23 @@ struct SV<CURAST_POS_U16> {
     uint2 q;
 };
 
-template <int PF, int IF>
+// KEEP: L2 evict-last hint for the vertex gathers — a grid row's vertices
+// are read again by the next row's chunk, while the index and queue streams
+// around them are evict-first (B 0.659 -> 0.653 ms stage 1, E200 3.61 ->
+// 3.54 ms; D unchanged)
+template <int PF, int IF, bool KEEP = true>
 __device__ __forceinline__ SV<PF> sv_load(const ItemGeo<PF, IF> &G, uint32_t v) {
     SV<PF> s;
     if constexpr (PF == CURAST_POS_U16) {
         s.q = __ldg((const uint2 *)G.pos + v);
+    } else if constexpr (KEEP) {
+        uint64_t pol;
+        asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        float4 q;
+        asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+            : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w)
+            : "l"((const float4 *)G.pos + v), "l"(pol));
+        s.p = make_float3(q.x, q.y, q.z);
     } else {
         const float4 q = __ldg((const float4 *)G.pos + v);
         s.p = make_float3(q.x, q.y, q.z);
