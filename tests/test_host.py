@@ -427,3 +427,55 @@ def test_row_raster_choice_follows_fragments_per_triangle():
     assert choose(9_331_200, 4_666_508) == 0
     assert choose(7_097_009, 2_276_079) == 0
     assert choose(0, 0) == 0
+
+
+def test_c_abi_rejects_invalid_frames_before_any_launch():
+    """The C ABI validates a frame on the host and returns CURAST_E_INVALID
+    with a message before touching the device (no GPU needed): resolution
+    limits, tile size, filter without rows, stage-1 work tables, chunk sizes,
+    the fp64 queue and the 2^22-item limit of the queue tags."""
+    import ctypes
+    from paper_2604_21749_b200 import _native as N
+    L = N.lib()
+    dummy = ctypes.c_void_p(0x1000)        # never dereferenced on these paths
+
+    def base():
+        f = N.CurastFrame()
+        f.fb = dummy
+        f.counters = dummy
+        f.width, f.height, f.tile_px = 64, 48, 64
+        f.n_units = 1
+        f.unit_chunk_prefix = dummy
+        f.unit_index = dummy
+        f.chunk_tris = 128
+        f.qx = dummy
+        f.qx_cap = 1024
+        f.n_items = 1
+        return f
+
+    def err(f, fn=L.curast_stage1):
+        rc = fn(ctypes.byref(f), None)
+        return rc, L.curast_last_error().decode()
+
+    cases = [
+        (dict(width=1 << 16, height=1 << 15), "resolution"),
+        (dict(tile_px=0), "tile_px"),
+        (dict(tile_px=5000), "tile_px"),
+        (dict(use_filter=1), "item_filter"),
+        (dict(unit_chunk_prefix=None), "work table"),
+        (dict(chunk_tris=100), "chunk_tris"),
+        (dict(chunk_tris=4096), "chunk_tris"),
+        (dict(qx=None), "fp64 queue"),
+        (dict(qx_cap=1 << 32), "2^32"),
+        (dict(n_items=1 << 22), "2^22"),
+    ]
+    for fields, needle in cases:
+        f = base()
+        for k, v in fields.items():
+            setattr(f, k, v)
+        rc, msg = err(f)
+        assert rc == -1, (fields, rc, msg)
+        assert needle in msg, (fields, msg)
+    f = base()
+    f.fb = None
+    assert err(f, L.curast_frame_clear)[0] == -1
