@@ -207,11 +207,35 @@ def device_mesh(mesh, device) -> DeviceMesh:
     return dm
 
 
+class _MeshSlice:
+    """A generated mesh's place in a streamed SceneGeometry: the DeviceMesh
+    metadata the host needs (formats, bounds, codec parameters) and views of
+    its slice of the concatenated buffers."""
+
+    def __init__(self, dm, positions, indices):
+        for k in ("pos_format", "vertex_count", "triangle_count", "qgrid", "pos_bound",
+                  "idx_format", "pack", "device"):
+            setattr(self, k, getattr(dm, k))
+        self.positions = positions
+        self.indices = indices
+
+
+def _packed_words(mesh) -> int:
+    """int32 words of generators.DeviceGeneratedMesh.generate_compressed."""
+    V = mesh.vertex_count()
+    b = max(1, int(V - 1).bit_length())
+    return (3 * int(mesh.triangle_count) * b + 31) // 32 + 1 + 2
+
+
 class SceneGeometry:
     """Concatenation of the draw list's unique meshes in one device format,
     in first-appearance order (pipeline.py:103-111)."""
 
     def __init__(self, meshes: list, device):
+        if (len(meshes) > 1 and all(hasattr(m, "generate") for m in meshes)
+                and len({bool(getattr(m, "compressed", False)) for m in meshes}) == 1):
+            self._streamed(meshes, device)
+            return
         dms = [device_mesh(m, device) for m in meshes]
         self.meshes = dms
         pfs = {d.pos_format for d in dms}
@@ -247,6 +271,40 @@ class SceneGeometry:
             self.positions = torch.cat(pos_parts)
             self.indices = torch.cat(idx_parts)
         self.keepalive = dms
+
+    def _streamed(self, meshes: list, device):
+        """Generated meshes (config E) go straight into preallocated
+        concatenated buffers, one at a time: peak memory is the scene plus
+        one mesh, instead of every mesh's own copy plus the concatenation
+        (which did not fit a 4-GPU shard of E, ~89 GB per GPU)."""
+        comp = bool(getattr(meshes[0], "compressed", False))
+        nvs = [int(m.vertex_count()) for m in meshes]
+        if comp:
+            nis = [_packed_words(m) for m in meshes]
+            self.positions = torch.empty((sum(nvs), 4), dtype=torch.int16, device=device)
+            self.pos_format, self.idx_format = N.POS_U16, N.IDX_PACKED
+        else:
+            nis = [-(-3 * int(m.triangle_count) // 4) * 4 for m in meshes]
+            self.positions = torch.empty((sum(nvs), 4), dtype=torch.float32, device=device)
+            self.pos_format, self.idx_format = N.POS_F32, N.IDX_U32
+        self.indices = torch.zeros(sum(nis), dtype=torch.int32, device=device)
+        self.vtx_off, self.idx_off, self.meshes = [], [], []
+        nv = ni = 0
+        for m, v, i in zip(meshes, nvs, nis):
+            dm = DeviceMesh(m, device)               # transient, not cached on the mesh
+            pv = self.positions[nv:nv + v]
+            pv.copy_(dm.positions.reshape(v, 4))
+            ix = dm.indices.reshape(-1)
+            iv = self.indices[ni:ni + i]
+            iv[:ix.numel()].copy_(ix)
+            self.vtx_off.append(nv)
+            self.idx_off.append(ni)
+            self.meshes.append(_MeshSlice(dm, pv, iv))
+            del dm, ix
+            nv += v
+            ni += i
+        self.positions = self.positions.reshape(-1)
+        self.keepalive = []
 
 
 _scene_cache: dict = {}
