@@ -24,6 +24,10 @@ def child(config, K):
     import paper_2604_21749_b200 as cr
     from paper_2604_21749_b200.pipeline import PreparedFrame
     from frame_once import scene_for
+    if os.environ.get("AB_CHUNK"):                       # override the host's chunk choice
+        import paper_2604_21749_b200.pipeline as _pl
+        _c = int(os.environ["AB_CHUNK"])
+        _pl._choose_chunk = lambda work, cmax, q, target: _c
     scene, cam = scene_for(config)
     dl = cr.build_draw_list(scene, cam)
     pf = PreparedFrame(dl, cam, cr.RasterConfig(), fresh_fb=False)
