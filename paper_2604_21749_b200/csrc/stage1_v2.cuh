@@ -515,8 +515,11 @@ __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (
     // the decisions of all instances first (need / frustum bits of
     // instance k in bits 4k..4k+3, interior flag in bit k), then one
     // reservation and the queue writes of the whole step
-    unsigned long long needm = 0, frm = 0;
-    unsigned intm = 0;
+    // need bits of instances 0-7 / 8-15 in two words (the instance index is
+    // warp-uniform, so the half is a uniform branch, not a 64-bit shift);
+    // frustum outcomes are only counted
+    unsigned need_lo = 0, need_hi = 0, intm = 0;
+    int nfr = 0;
 #pragma unroll 1
     for (int k = 0; k < ninst; ++k) {
         LeanConsts F;
@@ -525,11 +528,13 @@ __device__ __forceinline__ void v2i_step(const curast_frame_t &f, const float4 (
 #pragma unroll
         for (int j = 0; j < 6; ++j) v[j] = pv_project(F, sv_pos(G, sv[j]));
         const unsigned bits = strip_bits<KIND, true>(F, v, W, H, slack, tiny);
-        needm |= (unsigned long long)(bits & vmask) << (4 * k);
-        frm |= (unsigned long long)((bits >> 4) & vmask) << (4 * k);
+        if (k < 8) need_lo |= (bits & vmask) << (4 * k);
+        else need_hi |= (bits & vmask) << (4 * (k - 8));
+        nfr += __popc((bits >> 4) & vmask);
         intm |= ((bits >> 8) & 1u) << k;
     }
-    const int nneed = __popcll(needm), nfr = __popcll(frm);
+    unsigned long long needm = ((unsigned long long)need_hi << 32) | need_lo;
+    const int nneed = __popcll(needm);
     cnt16 += (unsigned)nfr + ((unsigned)(nv * ninst - nneed - nfr) << 16);
     // warp prefix sum of the per-lane entry counts
     int incl = nneed;
