@@ -345,7 +345,8 @@ def filter_rows(item_mv: np.ndarray, pos_bound: np.ndarray, p0: float, p1: float
 
     X = px*d = A*vx + B*d, Y = py*d = Dh*d - C*vy, d = -vz with
     A = W/2*p0, B = W/2, C = H/2*p1, Dh = H/2 (kernels.py:78-96 rearranged).
-    Error bounds E = 16u * sum |term| over the item's position box."""
+    Error bounds E = E_FACTOR[pos_format] * u * sum |term| over the item's position box
+    (6 / 7 / 10 u for f32 / f64 / u16 positions, see E_FACTOR)."""
     n = len(item_mv)
     m = item_mv.reshape(n, 3, 4)
     A = 0.5 * width * p0
